@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 L3 batch decoder (BASELINE.json metric: decoded Mpixel/s and
+images/s per B200 at 1/2/4/8 GPUs, % of HBM roofline).
+
+Default workload = BASELINE.json configs[2] (the north_star target): Cityscapes-shaped
+32 x 2048x1024 RGB8, L3 patch N=128 (policy), synthetic content calibrated to Table 4's
+Cityscapes ratio 0.44, decode + fused normalise to fp32 NCHW. A "step" = one
+l3_decode_batch call over one batch (parse a1 + persistent decode a2-a7).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3_cityscapes|c2_imagenet|c4_uhd]
+                    [--out f32|u8] [--impl reference]
+
+Multi-GPU (N>1) is launched by torchrun: images are sharded per rank (weak scaling, no
+collective on the decode path; NCCL only for barrier + max-of-elapsed outside timing).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import l3synth  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+ROTATE = 4
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3_cityscapes", choices=["c3_cityscapes", "c2_imagenet", "c4_uhd"])
+    ap.add_argument("--out", default=None, choices=["f32", "u8"], help="default: f32 for c3, u8 otherwise")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_desc(config, out):
+    return {
+        "c3_cityscapes": "Cityscapes-shaped 32 x 2048x1024 RGB8, L3 N=128, synthetic ratio ~0.44 (Table 4)",
+        "c2_imagenet": "ImageNet-shaped 256 x ~500x375 RGB8 (variable), L3 N=32, synthetic ratio ~0.64 (KITTI)",
+        "c4_uhd": "4K 16 x 3840x2160 RGB8, L3 N=128, synthetic ratio ~0.63 (RAISE-1K)",
+    }[config] + (", decode + fused normalise -> fp32 NCHW" if out == "f32" else ", decode -> u8 CHW")
+
+
+def rank_images(config, rank):
+    """Rank r's shard: the config's recipe with seeds offset by r * batch (distinct images per rank)."""
+    cfg = l3synth.CONFIGS[config]
+    n = cfg["n"]
+    shapes = l3synth.imagenet_shapes(n, seed=1 + rank) if cfg["shape"] is None else [cfg["shape"]] * n
+    gain = l3synth.GAIN[cfg["gain"]]
+    return [l3synth.natural(h, w, cfg["seed0"] + rank * n + i, gain) for i, (h, w) in enumerate(shapes)]
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle", 0x100: "display_clock"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def cpu_baseline(files_host, offsets, shapes, pixels_per_image, target_cpu_s=15.0):
+    """The C oracle's batch decode (as it stands) on all host cores, on a bounded sample."""
+    from oracle import l3ref
+    threads = os.cpu_count() or 1
+    n = len(shapes)
+    t0 = time.perf_counter()
+    _, st, _ = l3ref.decode_batch(files_host, offsets, shapes, threads=threads)
+    one = time.perf_counter() - t0
+    assert (st == 0).all()
+    reps = max(1, min(10, int(math.ceil(target_cpu_s / max(one * threads, 1e-3)))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        l3ref.decode_batch(files_host, offsets, shapes, threads=threads)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(n * pixels_per_image / dt / 1e6, 3), "unit": "Mpixel/s", "cores": threads,
+            "kind": "oracle", "images_per_s": round(n / dt, 2),
+            "sample": f"{reps} x the full batch of {n} images (same bytes as the GPU run), "
+                      f"oracle/l3ref.c l3ref_decode_batch over {threads} pthreads, wall {dt * 1e3:.1f} ms/batch"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import l3ref
+    out = args.out or ("f32" if args.config == "c3_cityscapes" else "u8")
+    cfg = l3synth.CONFIGS[args.config]
+    imgs = rank_images(args.config, 0)[:4]          # bounded sample: 4 images, one per step
+    files = [l3ref.encode(im) for im in imgs]
+    shapes_all = [im.shape[1:] for im in imgs]
+    threads = os.cpu_count() or 1
+    mean, std = (0.485, 0.456, 0.406), (0.229, 0.224, 0.225)
+
+    def step(i):
+        f = files[i % len(files)]
+        src = np.frombuffer(f, np.uint8)
+        offs = np.array([0, len(f)], np.uint64)
+        sh = np.array([shapes_all[i % len(files)]], np.int32)
+        dec, st, _ = l3ref.decode_batch(src, offs, sh, threads=threads)
+        assert st[0] == 0
+        if out == "f32":
+            l3ref.normalize(dec[0], mean, std)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    dt = time.perf_counter() - t0
+    px = sum(h * w for h, w in shapes_all) / len(shapes_all)
+    value = args.steps * px / dt / 1e6
+    line = {"impl": "reference", "metric": "decoded Mpixel/s", "value": round(value, 3), "unit": "Mpixel/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config + ": " + workload_desc(args.config, out), "batch": cfg["n"],
+                       "out": out, "step": "one image of the workload per step"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": threads, "kind": "oracle",
+                             "sample": f"1 image per step, rotating over {len(files)} images; oracle "
+                                       f"l3ref_decode_batch over {threads} pthreads" +
+                                       (" + fp64 normalise" if out == "f32" else "")},
+            "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_08711_b200 import BatchDecoder, encode_batch, l3, normalize_constants
+    from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    out_kind = args.out or ("f32" if args.config == "c3_cityscapes" else "u8")
+    out_dtype = torch.float32 if out_kind == "f32" else torch.uint8
+
+    # ---- inputs: synthetic shard -> GPU encoder -> L3 files resident in HBM
+    imgs = rank_images(args.config, rank)
+    n = len(imgs)
+    shapes_np = np.array([im.shape[1:] for im in imgs], np.int32)
+    src0, offs = encode_batch(imgs, device=dev)
+    comp_bytes = int(offs[-1].item())
+    raw_bytes = int(sum(im.size for im in imgs))
+    pixels = int(sum(int(h) * int(w) for h, w in shapes_np))
+    # rotating copies at distinct addresses so consecutive steps never hit L2-resident input
+    srcs = [src0] + [src0.clone() for _ in range(ROTATE - 1)]
+    shapes = torch.from_numpy(shapes_np).to(dev)
+    sizes = 3 * shapes_np[:, 0].astype(np.int64) * shapes_np[:, 1].astype(np.int64)
+    dense = bool((shapes_np == shapes_np[0]).all())
+    out_offsets = None
+    if dense:
+        out = torch.empty((n, 3, int(shapes_np[0, 0]), int(shapes_np[0, 1])), dtype=out_dtype, device=dev)
+    else:
+        oo = np.zeros(n, np.int64)
+        oo[1:] = np.cumsum(sizes)[:-1]
+        out_offsets = torch.from_numpy(oo).to(dev)
+        out = torch.empty(int(sizes.sum()), dtype=out_dtype, device=dev)
+    scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD) if out_kind == "f32" else ((1, 1, 1), (0, 0, 0))
+    dec = BatchDecoder(n, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    args_list = [dec.args(s, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias) for s in srcs]
+
+    # ---- self-check (lossless round trip through the product encoder + decoder)
+    with torch.cuda.stream(stream):
+        u8 = torch.empty(int(sizes.sum()), dtype=torch.uint8, device=dev)
+        oo_t = out_offsets if out_offsets is not None else torch.from_numpy(
+            np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)).to(dev)
+        a = dec.args(srcs[0], offs, shapes, u8, out_offsets=oo_t)
+        l3.l3_decode_batch(a, stream)
+    stream.synchronize()
+    ok = bool((dec.status[:n] == 0).all().item())
+    flat_ref = torch.cat([torch.from_numpy(np.ascontiguousarray(im).reshape(-1)) for im in imgs]).to(dev)
+    ok = ok and bool(torch.equal(u8, flat_ref))
+    del u8, flat_ref
+    assert ok, "self-check failed: decode(encode(x)) != x"
+
+    # ---- warmup + timed region (device time with CUDA events on the launching stream)
+    for i in range(args.warmup):
+        l3.l3_decode_batch(args_list[i % ROTATE], stream)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    with sampler:
+        t_start.record(stream)
+        for i in range(args.steps):
+            a = args_list[i % ROTATE]
+            ev[i][0].record(stream)
+            l3.l3_parse_batch(a, stream)
+            ev[i][1].record(stream)
+            l3.l3_decode_units(a, stream)
+            ev[i][2].record(stream)
+        t_end.record(stream)
+        stream.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    decode_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    parse_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    status_ok = bool((dec.status[:n] == 0).all().item())
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        okt = torch.tensor([1 if status_ok else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        status_ok = bool(okt.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = world * pixels * args.steps / (total_ms / 1e3) / 1e6
+    images_per_s = world * n * args.steps / (total_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the persistent decode kernel)
+    out_bytes = int(sizes.sum()) * (4 if out_kind == "f32" else 1)
+    alg_bytes = comp_bytes + out_bytes
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (decode_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.config}_{out_kind}")
+
+    # ---- end to end through the public API with HOST buffers (pinned H2D + decode + status D2H)
+    host_src = srcs[0][:comp_bytes].cpu().pin_memory()
+    host_status = torch.empty(n, dtype=torch.int32).pin_memory()
+    dev_src = torch.empty(comp_bytes + 16, dtype=torch.uint8, device=dev)
+    a_e2e = dec.args(dev_src, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias)
+    for _ in range(2):
+        l3.l3_load_decode_batch(a_e2e, host_src, host_status, stream)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        l3.l3_load_decode_batch(a_e2e, host_src, host_status, stream)
+    e1.record(stream)
+    stream.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    assert (host_status == 0).all()
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * pixels * args.e2e_steps / (e2e_ms / 1e3) / 1e6
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        offs_h = offs.cpu().numpy().astype(np.uint64)
+        cpu = cpu_baseline(host_src.numpy(), offs_h, shapes_np, pixels / n)
+
+    if rank == 0:
+        clocks = sampler.summary()
+        line = {
+            "metric": "decoded Mpixel/s", "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": args.config + ": " + workload_desc(args.config, out_kind), "batch_per_gpu": n,
+                       "global_batch": n * world, "out": out_kind, "parallelism": f"dp{world} (images sharded per rank)",
+                       "compressed_bytes_per_gpu": comp_bytes, "compression_ratio": round(comp_bytes / raw_bytes, 4),
+                       "l2": f"inputs rotate over {ROTATE} copies ({ROTATE * comp_bytes / 1e6:.0f} MB) and the "
+                             f"{out_bytes / 1e6:.0f} MB output is rewritten every step (> {L2_BYTES >> 20} MB L2)"},
+            "images_per_s": round(images_per_s, 2),
+            "ms_parse": round(parse_ms, 4), "ms_decode": round(decode_ms, 4),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "l3_decode_kernel (a2-a7; timed with the a7 finaliser launch)",
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": comp_bytes,
+                    "d2h_bytes_per_step": 4 * n, "call": "l3_load_decode_batch (pinned host src -> HBM -> decode -> "
+                                                         "status to host)"},
+            "gpu_launches": args.steps * l3.l3_decode_kernels_per_call(),
+            "clocks": clocks,
+            "status_ok": status_ok, "self_check": ok,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,98 @@
+"""User-facing wrappers over the C ABI: buffer management, no arithmetic.
+
+* :class:`BatchDecoder` — owns the device workspace / status buffers of one
+  stream and decodes a batch of L3 files resident in HBM into a u8 or fp32
+  ``[n, 3, H, W]`` tensor (or per-image blocks of a flat tensor for mixed
+  shapes) with one ``l3_decode_batch`` call.
+* :func:`encode_batch` — converts planar uint8 images to L3 files with the GPU
+  encoder (``l3_encode_batch``), returning the concatenated files on device.
+* :func:`normalize_constants` — host-side float32 (scale, bias) with
+  ``y = fmaf(x, scale, bias) == (x/255 - mean)/std`` up to rounding.
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import l3
+
+IMAGENET_MEAN = (0.485, 0.456, 0.406)
+IMAGENET_STD = (0.229, 0.224, 0.225)
+
+
+def normalize_constants(mean: Sequence[float], std: Sequence[float]):
+    """scale_c = 1/(255 std_c), bias_c = -mean_c/std_c, rounded once to float32."""
+    scale = tuple(float(np.float32(1.0 / (255.0 * s))) for s in std)
+    bias = tuple(float(np.float32(-m / s)) for m, s in zip(mean, std))
+    return scale, bias
+
+
+class BatchDecoder:
+    """Reusable decode context (workspace + status) for batches of up to `max_n` images."""
+
+    def __init__(self, max_n: int, device: torch.device | str = "cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("BatchDecoder needs a CUDA device (the decoder has no CPU path)")
+        self.device = torch.device(device)
+        self.max_n = max_n
+        ws = l3.l3_decode_workspace_size(max_n)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        self.status = torch.empty(max_n, dtype=torch.int32, device=self.device)
+        self.bad_unit = torch.empty(max_n, dtype=torch.int32, device=self.device)
+
+    def args(self, src, src_offsets, shapes, out, *, out_offsets=None, scale=(1.0, 1.0, 1.0),
+             bias=(0.0, 0.0, 0.0)):
+        n = int(shapes.shape[0])
+        if n > self.max_n:
+            raise ValueError(f"batch of {n} > max_n={self.max_n}")
+        return l3.make_decode_args(src, src_offsets, shapes, out, self.status[:n], self.workspace,
+                                   out_offsets=out_offsets, bad_unit=self.bad_unit[:n], scale=scale, bias=bias)
+
+    def decode(self, src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor,
+               out: torch.Tensor, *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0),
+               stream=None):
+        """Enqueue one batch decode on `stream`; returns (status, bad_unit) device views."""
+        a = self.args(src, src_offsets, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias)
+        l3.l3_decode_batch(a, stream)
+        n = int(shapes.shape[0])
+        return self.status[:n], self.bad_unit[:n]
+
+
+def pack_files(files: Sequence[bytes], device="cuda"):
+    """Concatenate L3 files into one 16-byte aligned device buffer + int64 offsets (n+1)."""
+    offs = np.zeros(len(files) + 1, np.int64)
+    offs[1:] = np.cumsum([len(f) for f in files])
+    host = np.frombuffer(b"".join(files), np.uint8) if offs[-1] else np.zeros(0, np.uint8)
+    src = torch.empty(max(int(offs[-1]), 1), dtype=torch.uint8, device=device)
+    if offs[-1]:
+        src[: int(offs[-1])].copy_(torch.from_numpy(host.copy()))
+    return src, torch.from_numpy(offs).to(device)
+
+
+def encode_batch(images: Sequence[np.ndarray] | Sequence[torch.Tensor], patch_sizes=None, device="cuda",
+                 stream=None):
+    """GPU-encode planar uint8 [3, H, W] images. Returns (src, src_offsets) on device."""
+    n = len(images)
+    shapes = np.array([tuple(im.shape[1:]) for im in images], np.int32).reshape(n, 2)
+    sizes = np.array([3 * int(h) * int(w) for h, w in shapes], np.int64)
+    img_off = np.zeros(n, np.uint64)
+    if n > 1:
+        img_off[1:] = np.cumsum(sizes)[:-1]
+    flat = torch.empty(max(int(sizes.sum()), 1), dtype=torch.uint8, device=device)
+    for im, o, s in zip(images, img_off, sizes):
+        t = im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im))
+        flat[int(o):int(o) + int(s)].copy_(t.reshape(-1), non_blocking=False)
+    nh = None if patch_sizes is None else np.ascontiguousarray(patch_sizes, np.int32)
+    cap = sum(l3.l3_encode_max_bytes(int(w), int(h), 0 if nh is None else int(nh[i]))
+              for i, (h, w) in enumerate(shapes))
+    dst = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
+    dst_offsets = torch.empty(n + 1, dtype=torch.int64, device=device)
+    ws = torch.empty(max(l3.l3_encode_workspace_size(shapes, nh), 256), dtype=torch.uint8, device=device)
+    l3.l3_encode_batch(flat, img_off, shapes, nh, dst, dst_offsets, ws, stream)
+    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    total = int(dst_offsets[-1].item())
+    src = torch.empty(max(total, 1), dtype=torch.uint8, device=device)
+    src[:total].copy_(dst[:total])
+    return src, dst_offsets

@@ -1,0 +1,331 @@
+// l3_encode.cu — sm_100a batch ENCODER.
+//
+// Offline dataset conversion on the GPU, byte-identical to the oracle's CPU
+// encoder under the same readings (C1 residual mod 256, C2 signed
+// base for residual rows, C3 tie order, C4 clamp-to-edge, C5 first row per
+// patch, C6 k >= 1, C8 MSB-first rows, byte-aligned patches, C9 container).
+// Not on the decode hot path; kept simple: one warp per (image, channel, patch)
+// unit, 1 column per lane per step.
+//
+//   E1 l3_enc_size_kernel   bytes of every unit (two-pass: sizes first)
+//   E2 l3_enc_scan_kernel   per image: unit offsets (exclusive scan) + file size
+//   E3 l3_enc_files_kernel  file offsets across the batch (single CTA scan)
+//   E4 l3_enc_pack_kernel   header + offset table + packed bitstream per unit
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "l3_internal.cuh"
+
+namespace l3 {
+
+struct EncDesc {
+  uint64_t img_off;     // byte offset of the planar image in `images`
+  uint64_t unit0;       // global index of this image's first unit
+  uint32_t W, H, N, gx, P;
+  uint32_t hdr;         // 13 + 12P (fits: P bounded by the host check)
+};
+
+struct EncWs {
+  EncDesc* desc;        // n
+  uint64_t* unit_prefix;  // n+1 (global unit index)
+  uint32_t* unit_bytes;   // total units
+  uint32_t* unit_off;     // total units (relative to the data section)
+  uint64_t* file_size;    // n
+  static uint64_t bytes(int n, uint64_t units) {
+    return align_up(sizeof(EncDesc) * (uint64_t)n, 256) + align_up(8ull * (n + 1), 256) +
+           2 * align_up(4ull * units, 256) + align_up(8ull * n, 256);
+  }
+  static EncWs at(void* ws, int n, uint64_t units) {
+    EncWs v;
+    char* p = (char*)ws;
+    v.desc = (EncDesc*)p; p += align_up(sizeof(EncDesc) * (uint64_t)n, 256);
+    v.unit_prefix = (uint64_t*)p; p += align_up(8ull * (n + 1), 256);
+    v.unit_bytes = (uint32_t*)p; p += align_up(4ull * units, 256);
+    v.unit_off = (uint32_t*)p; p += align_up(4ull * units, 256);
+    v.file_size = (uint64_t*)p;
+    return v;
+  }
+};
+
+struct EncParams {
+  const uint8_t* images;
+  int n;
+  uint64_t total_units;
+  uint8_t* dst;
+  uint64_t* dst_offsets;
+  EncWs ws;
+};
+
+__device__ __forceinline__ int find_image(const uint64_t* prefix, int n, uint64_t u) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+struct UnitGeom {
+  const uint8_t* plane;
+  uint32_t W, x0, y0, w, h;
+};
+
+__device__ __forceinline__ UnitGeom unit_geom(const EncParams& p, const EncDesc& d, uint32_t ul) {
+  UnitGeom g;
+  const uint32_t ch = ul / d.P, pp = ul % d.P;
+  g.plane = p.images + d.img_off + (uint64_t)ch * d.W * d.H;
+  g.W = d.W;
+  g.x0 = (pp % d.gx) * d.N;
+  g.y0 = (pp / d.gx) * d.N;
+  g.w = min(d.N, d.W - g.x0);
+  g.h = min(d.N, d.H - g.y0);
+  return g;
+}
+
+// Residual of column c in row r (row 0 unfiltered, C5).
+__device__ __forceinline__ int residual(const UnitGeom& g, uint32_t r, uint32_t c) {
+  const uint8_t* row = g.plane + (uint64_t)(g.y0 + r) * g.W + g.x0;
+  const int x = row[c];
+  if (r == 0) return x;
+  const uint8_t* up = row - g.W;
+  const int t = up[c];
+  const int tl = c > 0 ? up[c - 1] : t;
+  const int tr = c + 1 < g.w ? up[c + 1] : t;
+  return (x - paeth_pred(tl, t, tr)) & 0xFF;
+}
+
+// Row base-delta parameters (readings C2/C6); warp-collective.
+__device__ __forceinline__ void row_kb(const UnitGeom& g, uint32_t r, int lane, int* k, int* base) {
+  int mn = 1 << 20, mx = -(1 << 20);
+  for (uint32_t c = lane; c < g.w; c += 32) {
+    int v = residual(g, r, c);
+    if (r > 0 && v >= 128) v -= 256;
+    mn = min(mn, v);
+    mx = max(mx, v);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  const int span = mx - mn;
+  *k = span > 0 ? 32 - __clz(span) : 1;
+  *base = mn & 0xFF;
+}
+
+__global__ void l3_enc_size_kernel(EncParams p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < p.total_units; u += warps) {
+    const int i = find_image(p.ws.unit_prefix, p.n, u);
+    const EncDesc d = p.ws.desc[i];
+    const UnitGeom g = unit_geom(p, d, (uint32_t)(u - d.unit0));
+    uint64_t bits = 0;
+    for (uint32_t r = 0; r < g.h; r++) {
+      int k, base;
+      row_kb(g, r, lane, &k, &base);
+      bits += 12u + (uint64_t)k * g.w;
+    }
+    if (lane == 0) p.ws.unit_bytes[u] = (uint32_t)((bits + 7) / 8);
+  }
+}
+
+// One CTA per image: exclusive scan of its units' byte counts.
+__global__ void __launch_bounds__(1024) l3_enc_scan_kernel(EncParams p) {
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t carry_s;
+  const int i = blockIdx.x;
+  const EncDesc d = p.ws.desc[i];
+  const uint64_t nu = 3ull * d.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (uint64_t b = 0; b < nu; b += blockDim.x) {
+    const uint64_t u = b + threadIdx.x;
+    const uint64_t v = u < nu ? p.ws.unit_bytes[d.unit0 + u] : 0;
+    uint64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t wv = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0, z = wv;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      warp_tot[lane] = z - wv;
+    }
+    __syncthreads();
+    const uint64_t excl = carry_s + warp_tot[wid] + x - v;
+    if (u < nu) p.ws.unit_off[d.unit0 + u] = (uint32_t)excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.ws.file_size[i] = (uint64_t)d.hdr + carry_s;
+}
+
+__global__ void l3_enc_files_kernel(EncParams p) {
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int i = 0; i < p.n; i++) {
+      p.dst_offsets[i] = acc;
+      acc += p.ws.file_size[i];
+    }
+    p.dst_offsets[p.n] = acc;
+  }
+}
+
+__device__ __forceinline__ void or_byte(uint32_t* words, uint32_t byte, uint32_t v) {
+  if (v) atomicOr(&words[byte >> 2], v << ((byte & 3) * 8));
+}
+
+// Put `nbits` (<= 12) of `v` at bit position `pos` (MSB-first) into a zeroed byte buffer.
+__device__ __forceinline__ void put_bits(uint32_t* words, uint32_t pos, uint32_t v, uint32_t nbits) {
+  const uint32_t b0 = pos >> 3, sh = pos & 7;
+  const uint32_t win = v << (24 - sh - nbits);   // 24-bit big-endian window
+  or_byte(words, b0, (win >> 16) & 0xFF);
+  or_byte(words, b0 + 1, (win >> 8) & 0xFF);
+  or_byte(words, b0 + 2, win & 0xFF);
+}
+
+__global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
+  extern __shared__ uint32_t buf[];
+  const int lane = threadIdx.x & 31;
+  for (uint64_t u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+    const int i = find_image(p.ws.unit_prefix, p.n, u);
+    const EncDesc d = p.ws.desc[i];
+    const uint32_t ul = (uint32_t)(u - d.unit0);
+    const UnitGeom g = unit_geom(p, d, ul);
+    uint8_t* file = p.dst + p.dst_offsets[i];
+    const uint32_t nbytes = p.ws.unit_bytes[u];
+    const uint32_t off = p.ws.unit_off[u];
+    // container fields (Fig. 5; reading C9)
+    if (lane < 4) file[13 + 4ull * ul + lane] = (uint8_t)(off >> (8 * lane));
+    if (ul == 0 && lane < 13) {
+      uint8_t b;
+      if (lane < 4) b = (uint8_t)"L3IF"[lane];
+      else if (lane < 8) b = (uint8_t)(d.W >> (8 * (lane - 4)));
+      else if (lane < 12) b = (uint8_t)(d.H >> (8 * (lane - 8)));
+      else b = (uint8_t)d.N;
+      file[lane] = b;
+    }
+    const uint32_t words = (nbytes + 3) / 4;
+    for (uint32_t x = lane; x < words && x < smem_words; x += 32) buf[x] = 0;
+    __syncwarp();
+    uint32_t pos = 0;
+    for (uint32_t r = 0; r < g.h; r++) {
+      int k, base;
+      row_kb(g, r, lane, &k, &base);
+      if (lane == 0) put_bits(buf, pos, ((uint32_t)k << 8) | (uint32_t)base, 12);
+      for (uint32_t c = lane; c < g.w; c += 32) {
+        const uint32_t delta = (uint32_t)(residual(g, r, c) - base) & 0xFFu;
+        put_bits(buf, pos + 12u + c * (uint32_t)k, delta, (uint32_t)k);
+      }
+      pos += 12u + (uint32_t)k * g.w;
+    }
+    __syncwarp();
+    uint8_t* out = file + d.hdr + off;
+    const uint8_t* b8 = reinterpret_cast<const uint8_t*>(buf);
+    for (uint32_t x = lane; x < nbytes; x += 32) out[x] = b8[x];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static uint32_t policy_N(uint32_t W, uint32_t H) {
+  const uint64_t A = (uint64_t)W * H;
+  return A < 777600ull ? 32u : (A < 2073600ull ? 64u : 128u);
+}
+
+struct EncPlan {
+  std::vector<EncDesc> desc;
+  std::vector<uint64_t> prefix;
+  uint64_t units = 0;
+  uint64_t max_bytes = 0;
+  uint32_t worst_patch = 0;
+  bool ok = true;
+};
+
+static EncPlan plan_encode(const int32_t* shapes, const int32_t* n_host, int32_t n,
+                           const uint64_t* img_offsets) {
+  EncPlan pl;
+  pl.desc.resize(n);
+  pl.prefix.resize(n + 1);
+  pl.prefix[0] = 0;
+  for (int i = 0; i < n; i++) {
+    const int32_t H = shapes[2 * i], W = shapes[2 * i + 1];
+    int32_t N = n_host ? n_host[i] : 0;
+    if (H <= 0 || W <= 0 || N < 0 || N > 255) { pl.ok = false; return pl; }
+    if (N == 0) N = (int32_t)policy_N((uint32_t)W, (uint32_t)H);
+    EncDesc& d = pl.desc[i];
+    d.W = W; d.H = H; d.N = N;
+    d.gx = (W + N - 1) / N;
+    const uint64_t P = (uint64_t)d.gx * ((H + N - 1) / N);
+    if (3 * P >= (1ull << 29)) { pl.ok = false; return pl; }
+    d.P = (uint32_t)P;
+    d.hdr = (uint32_t)(13 + 12 * P);
+    d.img_off = img_offsets ? img_offsets[i] : 0;
+    d.unit0 = pl.prefix[i];
+    pl.prefix[i + 1] = pl.prefix[i] + 3 * P;
+    const uint32_t wn = (uint32_t)N;
+    const uint32_t worst = (wn * (12 + 8 * wn) + 7) / 8;
+    if (worst > pl.worst_patch) pl.worst_patch = worst;
+    pl.max_bytes += l3_encode_max_bytes((uint32_t)W, (uint32_t)H, N);
+  }
+  pl.units = pl.prefix[n];
+  return pl;
+}
+
+uint64_t encode_workspace_size(const int32_t* shapes, const int32_t* n_host, int32_t n) {
+  EncPlan pl = plan_encode(shapes, n_host, n, nullptr);
+  if (!pl.ok) return 0;
+  // descriptors + prefix are uploaded in front of the EncWs sections
+  return EncWs::bytes(n, pl.units);
+}
+
+l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s) {
+  if (!a || a->n < 0 || (a->n > 0 && (!a->images || !a->shapes_host || !a->img_offsets_host || !a->dst ||
+                                       !a->dst_offsets || !a->workspace)))
+    return L3_E_INVALID_ARGUMENT;
+  if (a->n == 0) return L3_OK;
+  EncPlan pl = plan_encode(a->shapes_host, a->n_host, a->n, a->img_offsets_host);
+  if (!pl.ok) return L3_E_INVALID_ARGUMENT;
+  if (a->workspace_bytes < EncWs::bytes(a->n, pl.units) || a->dst_capacity < pl.max_bytes)
+    return L3_E_INVALID_ARGUMENT;
+  EncWs ws = EncWs::at(a->workspace, a->n, pl.units);
+  if (cudaMemcpyAsync(ws.desc, pl.desc.data(), sizeof(EncDesc) * a->n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return L3_E_CUDA;
+  if (cudaMemcpyAsync(ws.unit_prefix, pl.prefix.data(), 8ull * (a->n + 1), cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return L3_E_CUDA;
+  if (pl.units == 0) return L3_OK;
+  EncParams p;
+  p.images = a->images;
+  p.n = a->n;
+  p.total_units = pl.units;
+  p.dst = a->dst;
+  p.dst_offsets = a->dst_offsets;
+  p.ws = ws;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (pl.units + 7) / 8;
+  const int grid1 = (int)(want < (uint64_t)sms * 16 ? (want ? want : 1) : (uint64_t)sms * 16);
+  l3_enc_size_kernel<<<grid1, 256, 0, s>>>(p);
+  l3_enc_scan_kernel<<<a->n, 1024, 0, s>>>(p);
+  l3_enc_files_kernel<<<1, 32, 0, s>>>(p);
+  const uint32_t smem_words = (pl.worst_patch + 16) / 4 + 1;
+  const size_t smem = (size_t)smem_words * 4;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(l3_enc_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return L3_E_CUDA;
+  const int grid4 = (int)(pl.units < (uint64_t)sms * 32 ? pl.units : (uint64_t)sms * 32);
+  l3_enc_pack_kernel<<<grid4, 32, smem, s>>>(p, smem_words);
+  return cudaGetLastError() == cudaSuccess ? L3_OK : L3_E_CUDA;
+}
+
+}  // namespace l3

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+u8 output must be bit-exact; fused fp32 output within 1e-6 absolute of the oracle's
+fp64 normalisation (BASELINE.json north_star); status / bad_unit identical to the
+oracle's sequential decode on corrupted input.
+"""
+import numpy as np
+import pytest
+import torch
+
+import l3synth
+from oracle import l3ref
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2208_08711_b200 import BatchDecoder, encode_batch, normalize_constants, pack_files  # noqa: E402
+from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD  # noqa: E402
+
+F32_TOL = 1e-6
+
+
+def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), canary=True, gap=0):
+    """Decode files on the GPU into per-image blocks (optionally separated by `gap` canary
+    elements). Returns (list of arrays [3,H,W], status, bad_unit, flat output)."""
+    src, offs = pack_files(files)
+    n = len(files)
+    sizes = [3 * h * w for h, w in shapes]
+    out_off = np.zeros(n, np.int64)
+    for i in range(1, n):
+        out_off[i] = out_off[i - 1] + sizes[i - 1] + gap
+    total = int(out_off[-1] + sizes[-1] + gap) if n else 1
+    fill = 0xA5 if dtype == torch.uint8 else float("nan")
+    out = torch.full((total,), fill, dtype=dtype, device="cuda")
+    dec = BatchDecoder(max(n, 1))
+    sh = torch.tensor(np.array(shapes, np.int32).reshape(n, 2), device="cuda")
+    st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(out_off).cuda(), scale=scale, bias=bias)
+    torch.cuda.synchronize()
+    flat = out.cpu().numpy()
+    imgs = [flat[int(o):int(o) + s].reshape(3, h, w) for o, s, (h, w) in zip(out_off, sizes, shapes)]
+    return imgs, st.cpu().numpy(), bad.cpu().numpy(), flat, out_off, sizes
+
+
+def check_u8(imgs_ref, files, gap=7):
+    shapes = [im.shape[1:] for im in imgs_ref]
+    got, st, bad, flat, out_off, sizes = gpu_decode(files, shapes, gap=gap)
+    assert st.tolist() == [0] * len(files), st
+    for i, (g, r) in enumerate(zip(got, imgs_ref)):
+        if not np.array_equal(g, r):
+            diff = np.argwhere(g != r)
+            raise AssertionError(f"image {i} shape {r.shape}: {len(diff)} mismatches, first {diff[:5].tolist()}")
+    # canary: gaps between images untouched -> every output byte written exactly where expected
+    mask = np.ones(flat.shape, bool)
+    for o, s in zip(out_off, sizes):
+        mask[int(o):int(o) + s] = False
+    assert (flat[mask] == 0xA5).all()
+
+
+# ------------------------------------------------------------------ configs
+
+def test_config1_64x64_gradient():
+    im = l3synth.make_batch("c1_64x64")[0]
+    f = l3ref.encode(im)
+    st, _, ref, _ = l3ref.decode(f)
+    assert st == 0
+    check_u8([ref], [f])
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (2, 2), (17, 31), (31, 17), (65, 129), (129, 65),
+                                   (33, 250), (300, 257)])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8, 16, 31, 32, 33, 64, 100, 127, 128, 129, 200, 255])
+def test_shapes_and_patch_sizes(shape, N):
+    H, W = shape
+    if N <= 3 and H * W > 4000:
+        pytest.skip("tiny N on large images: covered by smaller shapes")
+    imgs, files = [], []
+    for s in range(2):
+        im = l3synth.uniform_image(H, W, seed=1000 * N + s)
+        rule = l3ref.BASE_SIGNED if s == 0 else l3ref.BASE_UNSIGNED
+        files.append(l3ref.encode(im, N=N, base_rule=rule, k_extra=s))
+        st, _, ref, _ = l3ref.decode(files[-1])
+        assert st == 0
+        imgs.append(ref)
+    check_u8(imgs, files)
+
+
+def test_mixed_batch_many_shapes():
+    rng = np.random.default_rng(3)
+    imgs, files = [], []
+    for i in range(60):
+        H, W = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        N = int(rng.choice([0, 1, 7, 16, 32, 64, 128, 150, 255])) if H * W < 20000 else int(rng.choice([0, 32, 128]))
+        im = l3synth.uniform_image(H, W, seed=i)
+        files.append(l3ref.encode(im, N=N, k_extra=int(rng.integers(0, 3)) if i % 3 == 0 else 0))
+        imgs.append(im)
+    check_u8(imgs, files)
+
+
+def test_extremes_black_random():
+    imgs = [l3synth.black_image(1080, 1920), l3synth.random_image(1080, 1920, 0), l3synth.black_image(3, 5)]
+    check_u8(imgs, [l3ref.encode(im) for im in imgs])
+
+
+def test_config2_imagenet_batch():
+    imgs = l3synth.make_batch("c2_imagenet")
+    check_u8(imgs, [l3ref.encode(im) for im in imgs], gap=0)
+
+
+def test_config3_cityscapes_full_fp32_and_u8():
+    """Full config 3 batch (32 x 2048x1024), dense [n,3,H,W] output as bench.py runs it."""
+    imgs = l3synth.make_batch("c3_cityscapes")
+    files = [l3ref.encode(im) for im in imgs]
+    src, offs = pack_files(files)
+    n = len(imgs)
+    dec = BatchDecoder(n)
+    sh = torch.tensor([[1024, 2048]] * n, dtype=torch.int32, device="cuda")
+    out = torch.empty((n, 3, 1024, 2048), dtype=torch.uint8, device="cuda")
+    st, _ = dec.decode(src, offs, sh, out)
+    torch.cuda.synchronize()
+    assert st.cpu().tolist() == [0] * n
+    got = out.cpu().numpy()
+    for i in range(n):
+        st_o, _, ref, _ = l3ref.decode(files[i])
+        assert st_o == 0 and np.array_equal(got[i], ref), i
+    scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD)
+    outf = torch.empty((n, 3, 1024, 2048), dtype=torch.float32, device="cuda")
+    st, _ = dec.decode(src, offs, sh, outf, scale=scale, bias=bias)
+    torch.cuda.synchronize()
+    assert st.cpu().tolist() == [0] * n
+    # every image's sampled rows checked against the oracle's fp64 normalisation
+    rng = np.random.default_rng(0)
+    gf = outf.cpu().numpy()
+    for i in range(n):
+        rows = rng.integers(0, 1024, 16)
+        ref = l3ref.normalize(imgs[i][:, rows, :], IMAGENET_MEAN, IMAGENET_STD)
+        assert np.abs(gf[i][:, rows, :].astype(np.float64) - ref).max() <= F32_TOL
+    ref0 = l3ref.normalize(imgs[0], IMAGENET_MEAN, IMAGENET_STD)
+    assert np.abs(gf[0].astype(np.float64) - ref0).max() <= F32_TOL
+
+
+def test_config4_uhd_sampled():
+    imgs = l3synth.make_batch("c4_uhd", 3)
+    check_u8(imgs, [l3ref.encode(im) for im in imgs], gap=0)
+
+
+def test_fp32_all_values_and_ragged():
+    """All 256 byte values in every channel, odd widths (scalar-store path)."""
+    base = np.arange(256, dtype=np.uint8)
+    im = np.stack([np.tile(base, (3, 1)) for _ in range(3)])[:, :, :253]
+    im2 = l3synth.uniform_image(77, 333, 5)
+    files = [l3ref.encode(im, N=16), l3ref.encode(im2)]
+    scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD)
+    got, st, _, _, _, _ = gpu_decode(files, [im.shape[1:], im2.shape[1:]], torch.float32, scale, bias, gap=3)
+    assert st.tolist() == [0, 0]
+    for g, r in zip(got, [im, im2]):
+        ref = l3ref.normalize(r, IMAGENET_MEAN, IMAGENET_STD)
+        assert np.abs(g.astype(np.float64) - ref).max() <= F32_TOL
+
+
+# ------------------------------------------------------------------ faults (a7)
+
+def _corrupt_variants(rng, f, P):
+    data0 = 13 + 12 * 3 * P // 3
+    out = []
+    b = bytearray(f); b[0] ^= 0xFF; out.append(bytes(b))                     # magic
+    out.append(bytes(f[:10]))                                                # short header
+    out.append(bytes(f[:data0 - 1]))                                         # truncated offsets
+    out.append(bytes(f[:-int(rng.integers(1, 40))]))                         # truncated stream
+    b = bytearray(f); b[13 + 4 * 3:13 + 4 * 4] = b[13:17]; out.append(bytes(b))   # non-monotonic offsets
+    for _ in range(6):                                                       # random byte flips in data
+        b = bytearray(f)
+        for _ in range(int(rng.integers(1, 4))):
+            j = int(rng.integers(data0, len(b)))
+            b[j] = int(rng.integers(0, 256))
+        out.append(bytes(b))
+    b = bytearray(f)                                                         # k = 0 at a unit start
+    offs = np.frombuffer(bytes(f[13:data0]), "<u4")
+    u = int(rng.integers(0, len(offs)))
+    b[data0 + int(offs[u])] &= 0x0F
+    out.append(bytes(b))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fault_injection_status_parity(seed):
+    rng = np.random.default_rng(seed)
+    H, W = int(rng.integers(20, 200)), int(rng.integers(20, 300))
+    N = int(rng.choice([8, 16, 32, 64, 128, 200]))
+    im = l3synth.natural(H, W, seed, 3.0)
+    f = l3ref.encode(im, N=N)
+    P = (-(-W // N)) * (-(-H // N))
+    files = _corrupt_variants(rng, f, P) + [f]
+    shapes = [(H, W)] * len(files)
+    _, st, bad, _, _, _ = gpu_decode(files, shapes)
+    for i, fi in enumerate(files):
+        rst, rbad, _, _ = l3ref.decode(fi, exp_shape=(H, W))
+        assert (st[i], bad[i]) == (rst, rbad), (i, st[i], bad[i], rst, rbad)
+
+
+def test_shape_mismatch_is_corrupt_header():
+    im = l3synth.natural(40, 50, 1, 1.0)
+    f = l3ref.encode(im)
+    _, st, bad, _, _, _ = gpu_decode([f, f], [(40, 50), (40, 51)])
+    assert st.tolist() == [0, 3] and bad.tolist() == [-1, -1]
+
+
+# ------------------------------------------------------------------ GPU encoder (f4)
+
+@pytest.mark.parametrize("seed", range(4))
+def test_gpu_encoder_byte_identical(seed):
+    rng = np.random.default_rng(seed)
+    imgs, Ns = [], []
+    for i in range(12):
+        H, W = int(rng.integers(1, 260)), int(rng.integers(1, 260))
+        imgs.append(l3synth.uniform_image(H, W, 100 * seed + i))
+        Ns.append(int(rng.choice([0, 1, 5, 16, 32, 64, 128, 200, 255])) if H * W < 30000 else 0)
+    src, offs = encode_batch(imgs, patch_sizes=Ns)
+    torch.cuda.synchronize()
+    o = offs.cpu().numpy()
+    buf = src.cpu().numpy()
+    for i, (im, N) in enumerate(zip(imgs, Ns)):
+        want = l3ref.encode(im, N=N)
+        got = buf[o[i]:o[i + 1]].tobytes()
+        assert got == want, (i, im.shape, N, len(got), len(want))
+
+
+def test_gpu_encoder_config3_identical():
+    imgs = l3synth.make_batch("c3_cityscapes", 4)
+    src, offs = encode_batch(imgs)
+    o = offs.cpu().numpy()
+    buf = src.cpu().numpy()
+    for i, im in enumerate(imgs):
+        assert buf[o[i]:o[i + 1]].tobytes() == l3ref.encode(im)
