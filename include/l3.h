@@ -125,6 +125,13 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* args, const void* host_sr
 /* Number of kernels one l3_decode_batch call launches (for launch accounting). */
 int32_t l3_decode_kernels_per_call(void);
 
+/*
+ * Diagnostic: evaluates the decoder's device-side custom-Paeth predictor
+ * (Fig. 3; ties TL, T, TR) on all 2^24 triples.
+ * out: device, 2^24 bytes; out[TL<<16 | T<<8 | TR] = predicted byte.
+ */
+l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream);
+
 /* Human-readable name of a status code; never NULL. */
 const char* l3_status_string(int32_t status);
 

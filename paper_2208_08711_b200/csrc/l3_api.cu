@@ -8,6 +8,7 @@
 namespace l3 {
 cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s);
 cudaError_t launch_decode_units(const l3_decode_args* a, cudaStream_t s);
+cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s);
 uint64_t encode_workspace_size(const int32_t* shapes, const int32_t* n_host, int32_t n);
 l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s);
 }  // namespace l3
@@ -64,6 +65,11 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* a, const void* host_src, 
       cudaSuccess)
     return L3_E_CUDA;
   return L3_OK;
+}
+
+l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream) {
+  if (!out) return L3_E_INVALID_ARGUMENT;
+  return l3::launch_selftest_paeth(out, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
 const char* l3_status_string(int32_t s) {

@@ -156,6 +156,7 @@ struct DecodeParams {
   WsView ws;
   int cls;                  // 0: N <= 128 tasks, 1: N > 128 tasks
   int finalize;             // last CTA writes status / bad_unit
+  uint32_t key_scale;       // 128: predictor key scale, passed at run time (keeps key math on IMAD)
 };
 
 __device__ __forceinline__ uint32_t err_key(uint32_t unit, int code) {
@@ -490,6 +491,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   }
 }
 
+}  // namespace l3
+
+#include "l3_decode_fast.cuh"
+
+namespace l3 {
+
+// Exhaustive self-test of the pair-form predictor used by the fast kernel:
+// out[TL<<16 | T<<8 | TR] = paeth_pred2 result, two triples per thread.
+__global__ void l3_selftest_paeth_kernel(uint8_t* out, uint32_t K) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) * 2u;
+  if (i >= (1u << 24)) return;
+  const uint32_t a = i, b = i + 1;
+  const uint32_t tl = ((a >> 16) & 0xFFu) | (((b >> 16) & 0xFFu) << 16);
+  const uint32_t t = ((a >> 8) & 0xFFu) | (((b >> 8) & 0xFFu) << 16);
+  const uint32_t tr = (a & 0xFFu) | ((b & 0xFFu) << 16);
+  const uint32_t p2 = paeth_pred2(tl, t, tr, K);
+  out[a] = (uint8_t)(p2 & 0xFFu);
+  out[b] = (uint8_t)((p2 >> 16) & 0xFFu);
+  if ((p2 & 0xFF00FF00u) != 0u) out[a] = out[b] = 0xEE;   // pair form must keep bytes 1, 3 zero
+}
+
+cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
+  l3_selftest_paeth_kernel<<<(1u << 23) / 256, 256, 0, s>>>(out, 128u);
+  return cudaGetLastError();
+}
+
 // ============================================================== host launch
 static int g_sm_count = 0;
 static int g_occ[2][2] = {{0, 0}, {0, 0}};
@@ -520,6 +547,22 @@ static int occupancy() {
   return occ > 0 ? occ : 1;
 }
 
+template <bool F32>
+static int fast_occupancy() {
+  int occ = 0;
+  cudaFuncSetAttribute(l3_decode_fast_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fast_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_fast_kernel<F32>, kWarpsPerCta * 32,
+                                                fast_smem_bytes());
+  return occ > 0 ? occ : 1;
+}
+
+template <bool F32>
+static cudaError_t launch_fast(const DecodeParams& dp, int grid, cudaStream_t s) {
+  l3_decode_fast_kernel<F32><<<grid, kWarpsPerCta * 32, fast_smem_bytes(), s>>>(dp);
+  return cudaGetLastError();
+}
+
 cudaError_t ensure_device_info() {
   if (g_sm_count == 0) {
     int dev = 0;
@@ -527,8 +570,8 @@ cudaError_t ensure_device_info() {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    g_occ[0][0] = occupancy<1, false>();
-    g_occ[0][1] = occupancy<1, true>();
+    g_occ[0][0] = fast_occupancy<false>();
+    g_occ[0][1] = fast_occupancy<true>();
     g_occ[1][0] = occupancy<2, false>();
     g_occ[1][1] = occupancy<2, true>();
   }
@@ -565,12 +608,13 @@ cudaError_t launch_decode_units(const l3_decode_args* a, cudaStream_t s) {
   dp.status = a->status;
   dp.bad_unit = a->bad_unit;
   dp.ws = WsView::at(a->workspace, a->n);
+  dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
   // class 0: N <= 128, persistent grid = SMs x resident CTAs
   dp.cls = 0;
   dp.finalize = 0;
   const int grid0 = g_sm_count * g_occ[0][f32 ? 1 : 0];
-  e = f32 ? launch_decode<1, true>(dp, grid0, s) : launch_decode<1, false>(dp, grid0, s);
+  e = f32 ? launch_fast<true>(dp, grid0, s) : launch_fast<false>(dp, grid0, s);
   if (e != cudaSuccess) return e;
   // class 1: N > 128 (rare; exits at once when there are none) + a7 finalisation
   dp.cls = 1;

@@ -1,0 +1,466 @@
+// l3_decode_fast.cuh — the hot decode kernel for patch sizes N <= 128 (every
+// policy-chosen N). Included by l3_decode.cu.
+//
+// Same unit mapping as the generic kernel (one warp, or an L-lane segment of it,
+// per (image, channel, patch); 4 columns per lane), restructured for issue
+// efficiency — the kernel is integer-issue-bound, not HBM-bound, in its naive
+// form (profiles/ r1 ncu: 53 instructions per sample):
+//   * row 0 peeled (no per-row "first row" test), rows >= 1 in a tight loop;
+//   * the next row's 12-bit header is fetched while the current row computes;
+//   * one combined validity test per row (k in 1..8 and the row fits the unit),
+//     the exact error code is only worked out on the (rare) failing path;
+//   * patch-edge clamping costs one select per lane per row: columns >= w of
+//     a ragged patch carry "ghost" copies of column w-1, so TR of the last
+//     real column is T without per-sample tests (RAGGED instantiation only);
+//   * stream (G = 1) ring bookkeeping is a single compare per row; waiting,
+//     refilling and the wrap mirror live on a slow path;
+//   * ring reads are 2 x LDS (the second at +4, the mirror makes the wrap
+//     contiguous) + 2 x PRMT + 1 funnel shift.
+#pragma once
+
+namespace l3 {
+
+constexpr int kRingPitch = kRingBytes + 16;   // ring + 16-byte wrap mirror
+
+__host__ __device__ constexpr size_t fast_smem_bytes() {
+  return (size_t)kWarpsPerCta * kRingPitch + (size_t)kWarpsPerCta * kSlots * 8 + 16;
+}
+
+// 32 stream bits at unwrapped ring bit position `bit` (MSB-first, reading C8).
+// Ring words are byte-swapped once when their chunk lands (swap_words), so a
+// word's bit 31 is the first stream bit of that word.
+__device__ __forceinline__ uint32_t rbits(const uint8_t* ring, uint32_t bit) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(ring + ((bit >> 3) & (uint32_t)(kRingBytes - 4)));
+  const uint32_t hi = p[0];
+  const uint32_t lo = p[1];   // at the ring end this is the mirror of word 0
+  uint32_t d;
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(bit));   // wraps the shift mod 32
+  return d;
+}
+
+// Byte-swap the 16-byte-aligned ring bytes [lo, hi) in place (lanes stride `step` x 16 B).
+__device__ __forceinline__ void swap_words(uint8_t* base, uint32_t lo, uint32_t hi, uint32_t first, uint32_t step) {
+  for (uint32_t x = lo + first * 16u; x < hi; x += step * 16u) {
+    uint4 v = *reinterpret_cast<uint4*>(base + x);
+    v.x = bswap32(v.x);
+    v.y = bswap32(v.y);
+    v.z = bswap32(v.z);
+    v.w = bswap32(v.w);
+    *reinterpret_cast<uint4*>(base + x) = v;
+  }
+}
+
+// Per-warp stream state (G == 1 tasks); warp-uniform.
+struct StreamState {
+  uint64_t A;           // absolute, 16-aligned start of the staged range
+  uint64_t B;           // absolute, 16-aligned end of the staged range
+  uint64_t stage_end;   // absolute end of the bytes that matter
+  uint32_t nchunks, issued, landed;
+  uint32_t landed_end;  // A-relative bytes known to be resident (0xFFFFFFFF = all)
+};
+
+__device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
+                                             uint64_t* bars, int lane) {
+  const uint32_t c = s.issued;
+  const uint64_t ca = s.A + (uint64_t)c * kSlotBytes;
+  const uint64_t cb = min(ca + kSlotBytes, s.B);
+  stage_range(src, ca, cb, lim, s.stage_end, ring + (c % kSlots) * kSlotBytes, &bars[c % kSlots], lane == 0, lane,
+              32);
+  s.issued = c + 1;
+}
+
+// Slow path of the per-row ring test: refill consumed slots, then wait until
+// `need` A-relative bytes are resident. Warp-collective.
+__device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
+                                            uint64_t* bars, uint32_t& phase_bits, uint32_t consumed_byte,
+                                            uint32_t need, int lane) {
+  const uint32_t consumed = consumed_byte / kSlotBytes;
+  if (s.issued < s.nchunks && s.issued < consumed + kSlots) {
+    __syncwarp();
+    fence_proxy_async_smem();
+    while (s.issued < s.nchunks && s.issued < consumed + kSlots) stream_issue(src, lim, s, ring, bars, lane);
+    __syncwarp();
+  }
+  while (s.landed < s.issued && (uint64_t)s.landed * kSlotBytes < need) {
+    const uint32_t sl = s.landed % kSlots;
+    mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
+    phase_bits ^= 1u << sl;
+    __syncwarp();
+    swap_words(ring, sl * kSlotBytes, (sl + 1) * kSlotBytes, lane, 32);
+    __syncwarp();
+    if (sl == 0) {   // keep the 16-byte mirror of word 0.. after the ring end current
+      if (lane < 4) reinterpret_cast<uint32_t*>(ring + kRingBytes)[lane] = reinterpret_cast<uint32_t*>(ring)[lane];
+      __syncwarp();
+    }
+    s.landed++;
+  }
+  s.landed_end = (s.landed == s.nchunks) ? 0xFFFFFFFFu : s.landed * kSlotBytes;
+}
+
+// ---------------------------------------------------------------- SWAR core
+// Two samples per 32-bit register, one per 16-bit half (value in the half's
+// low byte, high byte zero): "pair" form. Only native sm_100a SIMD ops are
+// used (VABSDIFF4.U8, VIMNMX.U16x2, VIMNMX3.U16x2, PRMT); the key arithmetic
+// runs on the FMA pipe (IMAD), relieving the half-rate ALU pipe that bounds
+// the scalar form (profiles/: ALU pipe 78% busy).
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t n) {   // clamped shift (PTX semantics)
+  uint32_t d;
+  asm("shr.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(n));
+  return d;
+}
+__device__ __forceinline__ uint32_t shl_c(uint32_t x, uint32_t n) {
+  uint32_t d;
+  asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(n));
+  return d;
+}
+
+// Custom Paeth predictor (Fig. 3; ties TL, T, TR — reading C3)
+// for two samples in pair form. With u = |TL-T|, v = |TR-T|, w = |TL-TR| the
+// distances to ref = TL+TR-T are d(TL) = v, d(T) = |TL+TR-2T| = 2max(u,v) - w,
+// d(TR) = u. Adding w to all three keeps the order and makes the
+// keys non-negative: k = (dist + w) << 7 | c, where the low bits c encode both
+// the tie rank and the byte index of that candidate in {X = [TL0,T0,TL1,T1],
+// Y = [TR0,0,TR1,0]}, so the minimum key's low nibbles are directly the PRMT
+// selector of the winner (keys <= 510 << 7 | 6 fit 16 bits).
+__device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_t tr, uint32_t K) {
+  const uint32_t u = __vabsdiffu4(tl, t);
+  const uint32_t v = __vabsdiffu4(tr, t);
+  const uint32_t w = __vabsdiffu4(tl, tr);
+  const uint32_t mx = __vmaxu2(u, v);
+  // K = 128 arrives as a runtime value so the key arithmetic stays on IMAD
+  // (FMA pipe) instead of LEA (ALU pipe). Low 7 bits: 0x50 | byte index; the 5
+  // in bits 4-6 makes the unused PRMT nibbles (1 and 3) pick byte 5 = 0 (or its
+  // sign, also 0), so the result's bytes 1 and 3 are zero.
+  const uint32_t kTL = v * K + (w * K + 0x00520050u);   // candidate bytes: s0 -> 0, s1 -> 2
+  const uint32_t kTR = u * K + (w * K + 0x00560054u);   // s0 -> 4, s1 -> 6
+  const uint32_t kT = mx * (2u * K) + 0x00530051u;      // s0 -> 1, s1 -> 3
+  const uint32_t m = __vimin3_u16x2(kTL, kT, kTR);
+  const uint32_t X = prmt(tl, t, 0x6240);
+  const uint32_t sel = prmt(m, 0, 0x4420);   // nibble0 <- half0 code, nibble2 <- half1 code
+  return prmt(X, tr, sel);                   // pair form: bytes 1 and 3 are zero
+}
+
+// Row reconstruction state of one lane: 4 consecutive columns j4..j4+3.
+struct LaneRows {
+  uint32_t bp;        // unwrapped ring bit position of the current row header
+  uint32_t lim;       // bit limit of the unit (same origin as bp)
+  uint32_t w;         // unit width
+  uint32_t h;         // unit height (0: inactive lane)
+  uint32_t j4;        // first column of this lane
+  uint32_t raw;       // the 32 stream bits starting at the current row header
+  uint32_t kacc;      // max over rows of (raw - 2^28): >= 2^31 iff some k was 0 or > 8
+  bool first, last, valid;
+  uint8_t* optr;      // output of column j4 in the current row
+  uint32_t pitch;     // bytes between output rows
+  uint32_t A, B;      // previous row, pair form: A = (c0, c1), B = (c2, c3)
+};
+
+template <bool F32, bool FAST>
+__device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi) {
+  if (F32) {
+    const float v0 = fmaf((float)(xA & 0xFFFFu), sc, bi), v1 = fmaf((float)(xA >> 16), sc, bi);
+    const float v2 = fmaf((float)(xB & 0xFFFFu), sc, bi), v3 = fmaf((float)(xB >> 16), sc, bi);
+    float* o = reinterpret_cast<float*>(s.optr);
+    if (FAST) {
+      *reinterpret_cast<float4*>(o) = make_float4(v0, v1, v2, v3);
+    } else {
+      o[0] = v0;
+      if (s.j4 + 1 < s.w) o[1] = v1;
+      if (s.j4 + 2 < s.w) o[2] = v2;
+      if (s.j4 + 3 < s.w) o[3] = v3;
+    }
+  } else {
+    const uint32_t q = prmt(xA, xB, 0x6420);   // [c0, c1, c2, c3]
+    if (FAST) {
+      *reinterpret_cast<uint32_t*>(s.optr) = q;
+    } else {
+      uint8_t* o = s.optr;
+      o[0] = (uint8_t)q;
+      if (s.j4 + 1 < s.w) o[1] = (uint8_t)(q >> 8);
+      if (s.j4 + 2 < s.w) o[2] = (uint8_t)(q >> 16);
+      if (s.j4 + 3 < s.w) o[3] = (uint8_t)(q >> 24);
+    }
+  }
+}
+
+// One row of one lane (a3-a6). FIRST: row 0 of the patch (no prediction,
+// PAPER.md:139 "the first row is stored in a raw data format").
+// Validity is accumulated, not tested per row: kacc collects every row's k
+// (a k outside 1..8 sets its top bit) and a row overrunning the unit leaves
+// bp > lim after the patch (bp only grows). Decoding continues on garbage in
+// that case (reads stay inside the ring, writes inside the patch) and the
+// exact first error is re-derived after the patch (unit_first_error).
+// GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
+template <bool FIRST, bool F32, bool FAST, bool GUARD>
+__device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw, float sc,
+                                           float bi, uint32_t K) {
+  // a3: row header (PAPER.md:152 step 1): 4-bit k, 8-bit base
+  const uint32_t k = s.raw >> 28;
+  const uint32_t base2 = (s.raw >> 20) * 0x00010001u;   // (k:4 | base:8) per half; k bits masked below
+  const uint32_t rowbits = 12u + k * s.w;
+  const bool live = GUARD ? (r < s.h) : true;
+  const uint32_t nbp = s.bp + rowbits;
+  const uint32_t raw_next = rbits(ring, nbp);           // next row's header, fetched early
+  // a4: pixel-wise delta unpack (PAPER.md:152 step 2, :187): field = 4 k-bit deltas, MSB-first
+  const uint32_t field = rbits(ring, s.bp + 12u + s.j4 * k);
+  const uint32_t sh = 32u - k;
+  const uint32_t pk = shl_c(1u, k);
+  const uint32_t d0 = shr_c(field, sh);
+  const uint32_t d1 = shr_c(field * pk, sh);
+  const uint32_t d2 = shr_c(field * (pk * pk), sh);
+  const uint32_t d3 = shr_c(field * (pk * pk * pk), sh);
+  const uint32_t dA = d1 * 0x10000u + d0 + base2;
+  const uint32_t dB = d3 * 0x10000u + d2 + base2;
+  uint32_t xA, xB;
+  if (FIRST) {
+    xA = dA & 0x00FF00FFu;
+    xB = dB & 0x00FF00FFu;
+  } else {
+    // a5: row-wise parallel custom Paeth
+    const uint32_t Bl = __shfl_up_sync(0xffffffffu, s.B, 1, Lw);     // left lane's (c2, c3)
+    const uint32_t Ar = __shfl_down_sync(0xffffffffu, s.A, 1, Lw);   // right lane's (c0, c1)
+    const uint32_t LF = s.first ? (s.A << 16) : Bl;   // byte 2 = TL of column j4 (C4: T at column 0)
+    const uint32_t RT = s.last ? (s.B >> 16) : Ar;    // byte 0 = TR of column j4+3 (C4; ghosts when ragged)
+    const uint32_t TLA = prmt(LF, s.A, 0x5452);       // (c-1, c0)
+    const uint32_t TRA = prmt(s.A, s.B, 0x5412);      // (c1, c2) = TL of pair B
+    const uint32_t TRB = prmt(s.B, RT, 0x5412);       // (c3, c+4)
+    xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
+    xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
+  }
+  if (!FAST) {   // ragged patch: columns >= w are ghosts of column w-1
+    if (s.j4 + 1 >= s.w) xA = (xA & 0xFFu) * 0x00010001u;
+    if (s.j4 + 2 >= s.w) xB = (xA >> 16) * 0x00010001u;
+    if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
+  }
+  // a6: store (u8 planar, or fused cast + normalise)
+  if (live && s.valid) store4<F32, FAST>(s, xA, xB, sc, bi);
+  s.A = xA;
+  s.B = xB;
+  if (live) {
+    s.kacc = max(s.kacc, s.raw - 0x10000000u);
+    s.bp = nbp;
+    s.raw = raw_next;
+  }
+  s.optr += s.pitch;
+}
+
+template <bool F32, bool FAST, bool STREAM>
+__device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uint32_t hmax, uint32_t Lw, float sc,
+                                                 float bi, uint32_t K, const uint8_t* src, uint64_t lim,
+                                                 StreamState& st, uint64_t* bars, uint32_t& phase_bits,
+                                                 uint32_t rowmax, int lane) {
+  constexpr bool GUARD = !STREAM;   // G == 1: every lane runs exactly the unit's h rows
+  if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
+    stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
+  s.raw = rbits(ring, s.bp);
+  decode_row<true, F32, FAST, GUARD>(s, ring, 0, Lw, sc, bi, K);
+  uint32_t r = 1;
+  for (; r + 1 < hmax; r += 2) {   // two rows per ring test
+    if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
+      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
+    decode_row<false, F32, FAST, GUARD>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD>(s, ring, r + 1, Lw, sc, bi, K);
+  }
+  if (r < hmax) {
+    if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
+      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
+    decode_row<false, F32, FAST, GUARD>(s, ring, r, Lw, sc, bi, K);
+  }
+}
+
+// Exact first error of a unit whose row loop raised `err`, re-derived from the
+// compressed bytes in global memory with the sequential rules of a3/a7
+// (k = 0 or k > 8 -> CORRUPT_STREAM; too few bits -> TRUNCATED).
+__device__ __noinline__ int unit_first_error(const uint8_t* src, uint64_t start, uint64_t end, uint32_t w,
+                                             uint32_t h) {
+  const uint64_t len_bits = (end - start) * 8ull;
+  uint64_t pos = 0;
+  for (uint32_t r = 0; r < h; r++) {
+    if (len_bits - pos < 4) return L3_E_TRUNCATED_STREAM;
+    const uint64_t byte = start + (pos >> 3);
+    const uint32_t two = ((uint32_t)src[byte] << 8) | (byte + 1 < end ? (uint32_t)src[byte + 1] : 0u);
+    const uint32_t k = (two >> (12 - (pos & 7))) & 0xFu;
+    if (k == 0 || k > 8) return L3_E_CORRUPT_STREAM;
+    if (len_bits - pos < 12ull + (uint64_t)k * w) return L3_E_TRUNCATED_STREAM;
+    pos += 12ull + (uint64_t)k * w;
+  }
+  return L3_OK;
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    l3_decode_fast_kernel(DecodeParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * kRingPitch;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * kRingPitch) + warp * kSlots;
+  if (lane == 0) {
+    for (int s = 0; s < kSlots; s++) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t phase_bits = 0;
+
+  const uint64_t* prefix = p.ws.prefix[0];
+  const uint64_t total_tasks = prefix[p.n];
+  const uint64_t lim = p.src_offsets[p.n] & ~15ull;
+  const uint32_t K = p.key_scale;
+
+  uint64_t task = 0;
+  if (lane == 0) task = atomicAdd(&p.ws.head->next_task[0], 1ull);
+  task = __shfl_sync(0xffffffffu, task, 0);
+  while (task < total_tasks) {
+    int lo = 0, hi = p.n;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
+    }
+    const int img = lo;
+    const ImgDesc d = p.ws.desc[img];
+    const uint32_t t = (uint32_t)(task - prefix[img]);
+    // claim the next task now; the atomic's latency hides behind this one
+    uint64_t next = 0;
+    if (lane == 0) next = atomicAdd(&p.ws.head->next_task[0], 1ull);
+
+    const uint32_t G = d.G;
+    const bool stream = (G == 1);
+    const uint32_t Lw = stream ? 32u : d.L;            // G == 1: the unit spans the warp
+    const uint32_t seg = stream ? 0u : lane / Lw, j = stream ? (uint32_t)lane : lane % Lw;
+    const uint32_t nunits = 3u * d.P;
+    const uint32_t u = t * G + seg;
+    const uint8_t* file = p.src + d.file_off;
+
+    bool active = (seg < G) && (u < nunits);
+    uint32_t w = 0, h = 0, x0 = 0, y0 = 0, ch = 0;
+    uint64_t start = 0, end = 0;
+    if (active) {
+      ch = u / d.P;
+      const uint32_t pp = u - ch * d.P;
+      const uint32_t px = pp % d.gx, py = pp / d.gx;
+      x0 = px * d.N;
+      y0 = py * d.N;
+      w = min(d.N, d.W - x0);
+      h = min(d.N, d.H - y0);
+      const uint64_t off = ld_u32le(file + 13 + 4ull * u);
+      const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
+      if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
+        if (j == 0) atomicMin(&p.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+        active = false;
+      } else {
+        start = d.data_off + off;
+        end = d.data_off + nxt;
+      }
+    }
+    const uint32_t worst = active ? worst_patch_bytes(w, h) : 0u;
+    const uint64_t stage_end = active ? min(end, start + worst + 8) : 0;
+
+    LaneRows s;
+    s.w = w;
+    s.h = active ? h : 0u;
+    s.j4 = 4u * j;
+    s.first = (j == 0);
+    s.last = (s.j4 + 4u >= w);
+    s.valid = active && (s.j4 < w);
+    s.kacc = 0;
+    s.A = s.B = 0;
+    const uint32_t esz = F32 ? 4u : 1u;
+    const uint64_t elem = d.out_off + (uint64_t)ch * d.W * d.H + (uint64_t)y0 * d.W + x0 + s.j4;
+    s.optr = reinterpret_cast<uint8_t*>(p.out) + elem * esz;
+    s.pitch = d.W * esz;
+    const uint32_t len = active ? (uint32_t)min((uint64_t)(worst + 16), end - start) : 0u;
+
+    StreamState st;
+    st.landed_end = 0xFFFFFFFFu;
+    if (!stream) {
+      // whole-task staging: one aligned window per segment, one barrier (bars[0])
+      const uint32_t seg_bytes = kRingBytes / G;
+      uint32_t bytes = 0;
+      uint64_t a16 = 0, b16 = 0;
+      s.bp = 0;
+      if (active) {
+        a16 = start & ~15ull;
+        b16 = (stage_end + 15) & ~15ull;
+        const uint64_t be = b16 < lim ? b16 : lim;
+        bytes = be > a16 ? (uint32_t)(be - a16) : 0u;
+        s.bp = seg * seg_bytes * 8u + (uint32_t)(start - a16) * 8u;
+      }
+      uint32_t tx = (active && j == 0) ? bytes : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+      if (lane == 0) mbar_arrive_expect_tx(&bars[0], tx);
+      __syncwarp();
+      if (active) {
+        uint8_t* dst = ring + seg * seg_bytes;
+        if (j == 0 && bytes) bulk_g2s(dst, p.src + a16, bytes, &bars[0]);
+        const uint64_t t0 = a16 > lim ? a16 : lim;
+        for (uint64_t x = t0 + j; x < stage_end && x < b16; x += Lw) dst[x - a16] = __ldg(p.src + x);
+      }
+      mbar_wait(&bars[0], phase_bits & 1u);
+      phase_bits ^= 1u;
+      __syncwarp();
+      if (active) swap_words(ring + seg * seg_bytes, 0, (uint32_t)(b16 - a16), j, Lw);
+      __syncwarp();
+    } else {
+      // stream the unit through the ring: chunk i of [A, B) -> slot i % kSlots
+      st.A = start & ~15ull;
+      st.B = (stage_end + 15) & ~15ull;
+      st.stage_end = stage_end;
+      st.nchunks = active ? (uint32_t)((st.B - st.A + kSlotBytes - 1) / kSlotBytes) : 0u;
+      st.issued = 0;
+      st.landed = 0;
+      st.landed_end = 0;
+      const uint32_t first = min(st.nchunks, (uint32_t)kSlots);
+      while (st.issued < first) stream_issue(p.src, lim, st, ring, bars, lane);
+      __syncwarp();
+      s.bp = (uint32_t)(start - st.A) * 8u;
+    }
+    s.lim = s.bp + len * 8u;
+
+    uint32_t hmax = s.h;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    const bool fast_ok = !active || ((w & 3u) == 0 && ((reinterpret_cast<uintptr_t>(s.optr) & (F32 ? 15 : 3)) == 0) &&
+                                     ((s.pitch & (F32 ? 15u : 3u)) == 0));
+    const bool fast = __all_sync(0xffffffffu, fast_ok);
+    const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
+    const float bi = F32 ? (ch == 0 ? p.bias[0] : (ch == 1 ? p.bias[1] : p.bias[2])) : 0.f;
+    const uint32_t rowmax = (12u + 8u * 128u) / 8u + 10u;
+    if (hmax > 0) {
+      if (stream) {
+        if (fast)
+          decode_unit_rows<F32, true, true>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+        else
+          decode_unit_rows<F32, false, true>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+      } else {
+        if (fast)
+          decode_unit_rows<F32, true, false>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+        else
+          decode_unit_rows<F32, false, false>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+      }
+    }
+    const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
+    if (__any_sync(0xffffffffu, err) && err && j == 0) {   // a7: exact first error of a failed unit
+      const int code = unit_first_error(p.src, start, end, w, h);
+      if (code != L3_OK) atomicMin(&p.ws.errkey[img], err_key(u, code));
+    }
+    if (stream) {   // drain copies that were issued but never waited for
+      while (st.landed < st.issued) {
+        const uint32_t sl = st.landed % kSlots;
+        mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
+        phase_bits ^= 1u << sl;
+        st.landed++;
+      }
+    }
+    __syncwarp();
+    fence_proxy_async_smem();
+    task = __shfl_sync(0xffffffffu, next, 0);
+  }
+}
+
+}  // namespace l3

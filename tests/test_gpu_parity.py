@@ -233,3 +233,17 @@ def test_gpu_encoder_config3_identical():
     buf = src.cpu().numpy()
     for i, im in enumerate(imgs):
         assert buf[o[i]:o[i + 1]].tobytes() == l3ref.encode(im)
+
+
+def test_device_predictor_exhaustive_2_24():
+    """The kernel's pair-form (SWAR) predictor equals the oracle on all 2^24 triples."""
+    from paper_2208_08711_b200 import l3
+    out = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+    l3.l3_selftest_paeth(out)
+    torch.cuda.synchronize()
+    idx = np.arange(1 << 24, dtype=np.uint32)
+    ref = l3ref.predict_many((idx >> 16).astype(np.uint8), ((idx >> 8) & 255).astype(np.uint8),
+                             (idx & 255).astype(np.uint8))
+    got = out.cpu().numpy()
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, [(int(i) >> 16, (int(i) >> 8) & 255, int(i) & 255, int(got[i]), int(ref[i])) for i in bad[:8]]
