@@ -162,14 +162,17 @@ struct LaneRows {
 };
 
 template <bool F32, bool FAST>
-__device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi) {
+__device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi, bool pred) {
   if (F32) {
     const float v0 = fmaf((float)(xA & 0xFFFFu), sc, bi), v1 = fmaf((float)(xA >> 16), sc, bi);
     const float v2 = fmaf((float)(xB & 0xFFFFu), sc, bi), v3 = fmaf((float)(xB >> 16), sc, bi);
-    float* o = reinterpret_cast<float*>(s.optr);
-    if (FAST) {
-      *reinterpret_cast<float4*>(o) = make_float4(v0, v1, v2, v3);
-    } else {
+    if (FAST) {   // predicated STG.128, no branch
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+          "@p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(s.optr),
+          "f"(v0), "f"(v1), "f"(v2), "f"(v3), "r"((uint32_t)pred));
+    } else if (pred) {
+      float* o = reinterpret_cast<float*>(s.optr);
       o[0] = v0;
       if (s.j4 + 1 < s.w) o[1] = v1;
       if (s.j4 + 2 < s.w) o[2] = v2;
@@ -178,8 +181,10 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
   } else {
     const uint32_t q = prmt(xA, xB, 0x6420);   // [c0, c1, c2, c3]
     if (FAST) {
-      *reinterpret_cast<uint32_t*>(s.optr) = q;
-    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+          "@p st.global.b32 [%0], %1;\n\t}" ::"l"(s.optr), "r"(q), "r"((uint32_t)pred));
+    } else if (pred) {
       uint8_t* o = s.optr;
       o[0] = (uint8_t)q;
       if (s.j4 + 1 < s.w) o[1] = (uint8_t)(q >> 8);
@@ -198,8 +203,9 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
 // exact first error is re-derived after the patch (unit_first_error).
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
 template <bool FIRST, bool F32, bool FAST, bool GUARD>
-__device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw, float sc,
+__device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
+  const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
   // a3: row header (PAPER.md:152 step 1): 4-bit k, 8-bit base
   const uint32_t k = s.raw >> 28;
   const uint32_t base2 = (s.raw >> 20) * 0x00010001u;   // (k:4 | base:8) per half; k bits masked below
@@ -239,7 +245,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
   }
   // a6: store (u8 planar, or fused cast + normalise)
-  if (live && s.valid) store4<F32, FAST>(s, xA, xB, sc, bi);
+  store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
   s.A = xA;
   s.B = xB;
   if (live) {
