@@ -63,13 +63,16 @@ def workload_desc(config, out):
     }[config] + (", decode + fused normalise -> fp32 NCHW" if out == "f32" else ", decode -> u8 CHW")
 
 
-def rank_images(config, rank):
-    """Rank r's shard: the config's recipe with seeds offset by r * batch (distinct images per rank)."""
+def rank_images(config, rank, world=1):
+    """Rank r's shard of a synthetic dataset of world x batch images (weak scaling): image i of the
+    dataset uses seed seed0 + i; rank r takes shard_range(world * batch, r, world)."""
+    from paper_2208_08711_b200.parallel import shard_range
     cfg = l3synth.CONFIGS[config]
     n = cfg["n"]
-    shapes = l3synth.imagenet_shapes(n, seed=1 + rank) if cfg["shape"] is None else [cfg["shape"]] * n
+    idx = list(shard_range(n * world, rank, world))
+    shapes = l3synth.imagenet_shapes(n * world) if cfg["shape"] is None else [cfg["shape"]] * (n * world)
     gain = l3synth.GAIN[cfg["gain"]]
-    return [l3synth.natural(h, w, cfg["seed0"] + rank * n + i, gain) for i, (h, w) in enumerate(shapes)]
+    return [l3synth.natural(shapes[i][0], shapes[i][1], cfg["seed0"] + i, gain) for i in idx]
 
 
 class ClockSampler:
@@ -195,6 +198,7 @@ def main():
 
     from paper_2208_08711_b200 import BatchDecoder, encode_batch, l3, normalize_constants
     from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD
+    from paper_2208_08711_b200.parallel import aggregate_throughput, all_ranks_true, max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -207,7 +211,7 @@ def main():
     out_dtype = torch.float32 if out_kind == "f32" else torch.uint8
 
     # ---- inputs: synthetic shard -> GPU encoder -> L3 files resident in HBM
-    imgs = rank_images(args.config, rank)
+    imgs = rank_images(args.config, rank, world)
     n = len(imgs)
     shapes_np = np.array([im.shape[1:] for im in imgs], np.int32)
     src0, offs = encode_batch(imgs, device=dev)
@@ -272,17 +276,13 @@ def main():
     decode_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
     parse_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     status_ok = bool((dec.status[:n] == 0).all().item())
+    total_ms = max_over_ranks(total_ms)
+    status_ok = all_ranks_true(status_ok)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        okt = torch.tensor([1 if status_ok else 0], device=dev)
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        status_ok = bool(okt.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    value = world * pixels * args.steps / (total_ms / 1e3) / 1e6
-    images_per_s = world * n * args.steps / (total_ms / 1e3)
+    value = aggregate_throughput(pixels, world, args.steps, total_ms) / 1e6
+    images_per_s = aggregate_throughput(n, world, args.steps, total_ms)
 
     # ---- roofline of the dominant kernel (the persistent decode kernel)
     out_bytes = int(sizes.sum()) * (4 if out_kind == "f32" else 1)
@@ -312,11 +312,8 @@ def main():
     stream.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     assert (host_status == 0).all()
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * pixels * args.e2e_steps / (e2e_ms / 1e3) / 1e6
+    e2e_ms = max_over_ranks(e2e_ms)
+    e2e_value = aggregate_throughput(pixels, world, args.e2e_steps, e2e_ms) / 1e6
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
