@@ -76,7 +76,8 @@ typedef void* l3_stream_t;
  *   scale, bias  F32 only: per channel (R, G, B).
  *   status       device, n int32 (l3_status_t), written by the call.
  *   bad_unit     device, n int32 or NULL: first failing unit ch*P + p, else -1.
- *   workspace    device, >= l3_decode_workspace_size(n) bytes, 256-byte aligned.
+ *   workspace    device, >= l3_decode_workspace_size(n) bytes, 256-byte aligned,
+ *                zero-filled before first use (see l3_decode_batch).
  */
 typedef struct {
   const uint8_t* src;
@@ -98,18 +99,19 @@ typedef struct {
 uint64_t l3_decode_workspace_size(int32_t n);
 
 /*
- * The whole hot path, asynchronously on `stream`:
- * header parse + work decomposition, then the persistent patch decoder
- * (staging, row-header chain, delta unpack, row-parallel custom Paeth, store /
- * fused normalise), then the per-image status.
+ * The whole hot path as ONE persistent kernel
+ * launch, asynchronously on `stream`: header parse + work decomposition (by the
+ * first thread block), then the patch decoder on every SM (staging, row-header
+ * chain, delta unpack, row-parallel custom Paeth, store / fused normalise),
+ * then the per-image status (by the last thread block).
+ * The workspace must be zero-filled before its first use (e.g. cudaMemsetAsync);
+ * every call leaves it zero-filled again, so it can be reused without host work.
  */
 l3_status_t l3_decode_batch(const l3_decode_args* args, l3_stream_t stream);
 
-/* Step a1 alone (header parse, validation, work decomposition into workspace). */
+/* Step a1 alone (header validation, status of header-level errors, work
+ * decomposition into the workspace); decodes nothing. */
 l3_status_t l3_parse_batch(const l3_decode_args* args, l3_stream_t stream);
-
-/* Steps a2-a7 alone; requires l3_parse_batch with the same args earlier on `stream`. */
-l3_status_t l3_decode_units(const l3_decode_args* args, l3_stream_t stream);
 
 /*
  * Load + decode (PAPER.md:67 Load stage, :189 decode on its own stream):

@@ -38,7 +38,7 @@ class BatchDecoder:
         self.device = torch.device(device)
         self.max_n = max_n
         ws = l3.l3_decode_workspace_size(max_n)
-        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=self.device)   # zero before first use
         self.status = torch.empty(max_n, dtype=torch.int32, device=self.device)
         self.bad_unit = torch.empty(max_n, dtype=torch.int32, device=self.device)
 

@@ -7,7 +7,7 @@
 
 namespace l3 {
 cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s);
-cudaError_t launch_decode_units(const l3_decode_args* a, cudaStream_t s);
+cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s);
 cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s);
 uint64_t encode_workspace_size(const int32_t* shapes, const int32_t* n_host, int32_t n);
 l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s);
@@ -29,7 +29,7 @@ extern "C" {
 
 uint64_t l3_decode_workspace_size(int32_t n) { return n < 0 ? 0 : l3::WsView::bytes(n); }
 
-int32_t l3_decode_kernels_per_call(void) { return 3; }
+int32_t l3_decode_kernels_per_call(void) { return 1; }
 
 l3_status_t l3_parse_batch(const l3_decode_args* a, l3_stream_t stream) {
   l3_status_t st = check_decode_args(a);
@@ -37,17 +37,10 @@ l3_status_t l3_parse_batch(const l3_decode_args* a, l3_stream_t stream) {
   return l3::launch_parse(a, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
-l3_status_t l3_decode_units(const l3_decode_args* a, l3_stream_t stream) {
-  l3_status_t st = check_decode_args(a);
-  if (st != L3_OK || a->n == 0) return st;
-  return l3::launch_decode_units(a, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
-}
-
 l3_status_t l3_decode_batch(const l3_decode_args* a, l3_stream_t stream) {
   l3_status_t st = check_decode_args(a);
   if (st != L3_OK || a->n == 0) return st;
-  if (l3::launch_parse(a, (cudaStream_t)stream) != cudaSuccess) return L3_E_CUDA;
-  return l3::launch_decode_units(a, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
+  return l3::launch_decode_batch(a, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
 l3_status_t l3_load_decode_batch(const l3_decode_args* a, const void* host_src, uint64_t host_src_bytes,

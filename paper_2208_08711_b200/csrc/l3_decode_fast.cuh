@@ -22,6 +22,15 @@ namespace l3 {
 
 constexpr int kRingPitch = kRingBytes + 16;   // ring + 16-byte wrap mirror
 
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __host__ __device__ constexpr size_t fast_smem_bytes() {
   return (size_t)kWarpsPerCta * kRingPitch + (size_t)kWarpsPerCta * kSlots * 8 + 16;
 }
@@ -301,8 +310,10 @@ __device__ __noinline__ int unit_first_error(const uint8_t* src, uint64_t start,
 
 template <bool F32>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
-    l3_decode_fast_kernel(DecodeParams p) {
+    l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t sh_a[33], sh_b[33];
+  __shared__ unsigned int ticket;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * kRingPitch;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * kRingPitch) + warp * kSlots;
@@ -312,27 +323,43 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   }
   __syncwarp();
   uint32_t phase_bits = 0;
+  WsHead* head = p.pp.ws.head;
 
-  const uint64_t* prefix = p.ws.prefix[0];
-  const uint64_t total_tasks = prefix[p.n];
-  const uint64_t lim = p.src_offsets[p.n] & ~15ull;
+  // ---- a1 inside the persistent launch: CTA 0 parses every header and
+  // publishes the work decomposition; the other CTAs wait on the ready flag
+  // (CTA 0 is dispatched first, so the wait cannot starve it).
+  if (blockIdx.x == 0) {
+    parse_phase(p.pp, sh_a, sh_b);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
+  } else {
+    if (threadIdx.x == 0) {
+      while (ld_acquire_gpu(&head->ready) == 0u) __nanosleep(64);
+    }
+    __syncthreads();
+  }
+
+  const uint64_t* prefix = p.pp.ws.prefix[0];
+  const uint64_t total_tasks = prefix[p.pp.n];
+  const uint64_t lim = p.pp.src_offsets[p.pp.n] & ~15ull;
   const uint32_t K = p.key_scale;
 
   uint64_t task = 0;
-  if (lane == 0) task = atomicAdd(&p.ws.head->next_task[0], 1ull);
+  if (lane == 0) task = atomicAdd(&head->next_task[0], 1ull);
   task = __shfl_sync(0xffffffffu, task, 0);
   while (task < total_tasks) {
-    int lo = 0, hi = p.n;
+    int lo = 0, hi = p.pp.n;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
     }
     const int img = lo;
-    const ImgDesc d = p.ws.desc[img];
+    const ImgDesc d = p.pp.ws.desc[img];
     const uint32_t t = (uint32_t)(task - prefix[img]);
     // claim the next task now; the atomic's latency hides behind this one
     uint64_t next = 0;
-    if (lane == 0) next = atomicAdd(&p.ws.head->next_task[0], 1ull);
+    if (lane == 0) next = atomicAdd(&head->next_task[0], 1ull);
 
     const uint32_t G = d.G;
     const bool stream = (G == 1);
@@ -340,7 +367,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     const uint32_t seg = stream ? 0u : lane / Lw, j = stream ? (uint32_t)lane : lane % Lw;
     const uint32_t nunits = 3u * d.P;
     const uint32_t u = t * G + seg;
-    const uint8_t* file = p.src + d.file_off;
+    const uint8_t* file = p.pp.src + d.file_off;
 
     bool active = (seg < G) && (u < nunits);
     uint32_t w = 0, h = 0, x0 = 0, y0 = 0, ch = 0;
@@ -356,7 +383,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
       if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
-        if (j == 0) atomicMin(&p.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+        if (j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
         active = false;
       } else {
         start = d.data_off + off;
@@ -403,9 +430,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       __syncwarp();
       if (active) {
         uint8_t* dst = ring + seg * seg_bytes;
-        if (j == 0 && bytes) bulk_g2s(dst, p.src + a16, bytes, &bars[0]);
+        if (j == 0 && bytes) bulk_g2s(dst, p.pp.src + a16, bytes, &bars[0]);
         const uint64_t t0 = a16 > lim ? a16 : lim;
-        for (uint64_t x = t0 + j; x < stage_end && x < b16; x += Lw) dst[x - a16] = __ldg(p.src + x);
+        for (uint64_t x = t0 + j; x < stage_end && x < b16; x += Lw) dst[x - a16] = __ldg(p.pp.src + x);
       }
       mbar_wait(&bars[0], phase_bits & 1u);
       phase_bits ^= 1u;
@@ -422,7 +449,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       st.landed = 0;
       st.landed_end = 0;
       const uint32_t first = min(st.nchunks, (uint32_t)kSlots);
-      while (st.issued < first) stream_issue(p.src, lim, st, ring, bars, lane);
+      while (st.issued < first) stream_issue(p.pp.src, lim, st, ring, bars, lane);
       __syncwarp();
       s.bp = (uint32_t)(start - st.A) * 8u;
     }
@@ -440,20 +467,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     if (hmax > 0) {
       if (stream) {
         if (fast)
-          decode_unit_rows<F32, true, true>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, true>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, true>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, true>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       } else {
         if (fast)
-          decode_unit_rows<F32, true, false>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, false>(s, ring, hmax, Lw, sc, bi, K, p.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       }
     }
     const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
     if (__any_sync(0xffffffffu, err) && err && j == 0) {   // a7: exact first error of a failed unit
-      const int code = unit_first_error(p.src, start, end, w, h);
-      if (code != L3_OK) atomicMin(&p.ws.errkey[img], err_key(u, code));
+      const int code = unit_first_error(p.pp.src, start, end, w, h);
+      if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key(u, code));
     }
     if (stream) {   // drain copies that were issued but never waited for
       while (st.landed < st.issued) {
@@ -466,6 +493,47 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     __syncwarp();
     fence_proxy_async_smem();
     task = __shfl_sync(0xffffffffu, next, 0);
+  }
+
+  // ---- N > 128 units (never chosen by the policy): generic path, same ring
+  const uint64_t total1 = p.pp.ws.prefix[1][p.pp.n];
+  if (total1 > 0) {
+    for (;;) {
+      uint64_t t1 = 0;
+      if (lane == 0) t1 = atomicAdd(&head->next_task[1], 1ull);
+      t1 = __shfl_sync(0xffffffffu, t1, 0);
+      if (t1 >= total1) break;
+      phase_bits = generic_task<F32>(p, t1, ring, bars, phase_bits);
+    }
+  }
+
+  // ---- a7: per-image status, by the last CTA; it also re-zeroes the head so
+  // the workspace is ready for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    ticket = atomicAdd(&head->done_ctas, 1u);
+  }
+  __syncthreads();
+  if (ticket == gridDim.x - 1) {
+    __threadfence();
+    for (int i = threadIdx.x; i < p.pp.n; i += blockDim.x) {
+      if (p.pp.status[i] != L3_OK) continue;   // header-level error from a1
+      const uint32_t key = atomicAdd(&p.pp.ws.errkey[i], 0u);
+      if (key == kNoError) continue;
+      if (key == 0u) {
+        p.pp.status[i] = L3_E_CORRUPT_HEADER;
+      } else {
+        p.pp.status[i] = (key & 1u) ? L3_E_TRUNCATED_STREAM : L3_E_CORRUPT_STREAM;
+        if (p.pp.bad_unit) p.pp.bad_unit[i] = (int32_t)((key >> 1) & 0x3FFFFFFFu);
+      }
+    }
+    if (threadIdx.x == 0) {
+      head->next_task[0] = 0;
+      head->next_task[1] = 0;
+      head->done_ctas = 0;
+      head->ready = 0;
+    }
   }
 }
 

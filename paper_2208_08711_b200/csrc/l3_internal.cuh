@@ -36,10 +36,13 @@ struct ImgDesc {
 };
 
 // Workspace layout (256-byte aligned sections).
+// Zero-filled before first use; every decode launch leaves it zero-filled again
+// (the last CTA resets it), so the workspace is reusable without host work.
 struct WsHead {
   unsigned long long next_task[2];   // dynamic schedulers: [0] N <= 128, [1] N > 128
-  unsigned int done_ctas;            // last-CTA ticket of the finishing kernel
-  unsigned int pad[59];
+  unsigned int done_ctas;            // last-CTA ticket
+  unsigned int ready;                // 1 once CTA 0 has published the a1 results of this launch
+  unsigned int pad[58];
 };
 static_assert(sizeof(WsHead) == 256, "WsHead");
 

@@ -81,7 +81,7 @@ def lib() -> ctypes.CDLL:
                 raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
             L = ctypes.CDLL(LIB_PATH)
             P = ctypes.POINTER
-            for name in ("l3_decode_batch", "l3_parse_batch", "l3_decode_units"):
+            for name in ("l3_decode_batch", "l3_parse_batch"):
                 getattr(L, name).argtypes = [P(l3_decode_args), ctypes.c_void_p]
                 getattr(L, name).restype = ctypes.c_int
             L.l3_load_decode_batch.argtypes = [P(l3_decode_args), ctypes.c_void_p, ctypes.c_uint64,
@@ -107,7 +107,7 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED = ("l3_decode_workspace_size", "l3_decode_batch", "l3_parse_batch", "l3_decode_units",
+EXPORTED = ("l3_decode_workspace_size", "l3_decode_batch", "l3_parse_batch",
             "l3_load_decode_batch", "l3_decode_kernels_per_call", "l3_status_string", "l3_choose_patch_size",
             "l3_encode_max_bytes", "l3_encode_workspace_size", "l3_encode_batch", "l3_selftest_paeth")
 
@@ -173,10 +173,6 @@ def l3_decode_batch(args: l3_decode_args, stream=None) -> None:
 
 def l3_parse_batch(args: l3_decode_args, stream=None) -> None:
     _check("l3_parse_batch", lib().l3_parse_batch(ctypes.byref(args), _stream(stream)))
-
-
-def l3_decode_units(args: l3_decode_args, stream=None) -> None:
-    _check("l3_decode_units", lib().l3_decode_units(ctypes.byref(args), _stream(stream)))
 
 
 def l3_load_decode_batch(args: l3_decode_args, host_src: torch.Tensor, host_status: torch.Tensor,
