@@ -197,7 +197,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2208_08711_b200 import BatchDecoder, encode_batch, l3, normalize_constants
-    from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD
+    from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD, wide_hint
     from paper_2208_08711_b200.parallel import aggregate_throughput, all_ranks_true, max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -234,7 +234,9 @@ def main():
     scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD) if out_kind == "f32" else ((1, 1, 1), (0, 0, 0))
     dec = BatchDecoder(n, device=dev)
     stream = torch.cuda.Stream(device=dev)
-    args_list = [dec.args(s, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias) for s in srcs]
+    wide = wide_hint(shapes_np, out_dtype)
+    args_list = [dec.args(s, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide)
+                 for s in srcs]
 
     # ---- self-check (lossless round trip through the product encoder + decoder)
     with torch.cuda.stream(stream):
@@ -294,7 +296,7 @@ def main():
     host_src = srcs[0][:comp_bytes].cpu().pin_memory()
     host_status = torch.empty(n, dtype=torch.int32).pin_memory()
     dev_src = torch.empty(comp_bytes + 16, dtype=torch.uint8, device=dev)
-    a_e2e = dec.args(dev_src, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias)
+    a_e2e = dec.args(dev_src, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide)
     for _ in range(2):
         l3.l3_load_decode_batch(a_e2e, host_src, host_status, stream)
     stream.synchronize()

@@ -78,7 +78,13 @@ typedef void* l3_stream_t;
  *   bad_unit     device, n int32 or NULL: first failing unit ch*P + p, else -1.
  *   workspace    device, >= l3_decode_workspace_size(n) bytes, 256-byte aligned,
  *                zero-filled before first use (see l3_decode_batch).
+ *   flags        L3_DECODE_HINT_* performance hints (0 = none).
  */
+/* l3_decode_args.flags */
+#define L3_DECODE_HINT_WIDE 1u   /* u8 out: most files use 33 <= N <= 128 (e.g. policy N = 128 for
+                                    >= FHD images): pick the 8-column-per-lane kernel variant.
+                                    A performance hint only; every file decodes correctly either way. */
+
 typedef struct {
   const uint8_t* src;
   const uint64_t* src_offsets;
@@ -93,6 +99,8 @@ typedef struct {
   int32_t* bad_unit;
   void* workspace;
   uint64_t workspace_bytes;
+  uint32_t flags;   /* L3_DECODE_HINT_* bits, 0 = none */
+  uint32_t reserved;
 } l3_decode_args;
 
 /* Bytes of device workspace one l3_decode_batch call over n images needs. */

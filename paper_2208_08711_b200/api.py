@@ -22,6 +22,23 @@ IMAGENET_MEAN = (0.485, 0.456, 0.406)
 IMAGENET_STD = (0.229, 0.224, 0.225)
 
 
+def wide_hint(shapes_hw, out_dtype) -> bool:
+    """The L3_DECODE_HINT_WIDE choice for a batch (a performance hint only): u8 output, most images
+    large enough for the policy to pick N > 32 (>= 1080x720 pixels), and enough
+    patches (>= 16k units, e.g. 16 x UHD) that 2-patch tasks still keep every warp busy
+    (measured: wins on config 4, loses on 32 x 2048x1024)."""
+    if out_dtype != torch.uint8 or len(shapes_hw) == 0:
+        return False
+    big = 0
+    units = 0
+    for h, w in shapes_hw:
+        h, w = int(h), int(w)
+        n = 32 if h * w < 777600 else (64 if h * w < 2073600 else 128)
+        units += 3 * (-(-h // n)) * (-(-w // n))
+        big += h * w >= 1080 * 720
+    return 2 * big >= len(shapes_hw) and units >= 16384
+
+
 def normalize_constants(mean: Sequence[float], std: Sequence[float]):
     """scale_c = 1/(255 std_c), bias_c = -mean_c/std_c, rounded once to float32."""
     scale = tuple(float(np.float32(1.0 / (255.0 * s))) for s in std)
@@ -43,18 +60,20 @@ class BatchDecoder:
         self.bad_unit = torch.empty(max_n, dtype=torch.int32, device=self.device)
 
     def args(self, src, src_offsets, shapes, out, *, out_offsets=None, scale=(1.0, 1.0, 1.0),
-             bias=(0.0, 0.0, 0.0)):
+             bias=(0.0, 0.0, 0.0), wide=False):
         n = int(shapes.shape[0])
         if n > self.max_n:
             raise ValueError(f"batch of {n} > max_n={self.max_n}")
         return l3.make_decode_args(src, src_offsets, shapes, out, self.status[:n], self.workspace,
-                                   out_offsets=out_offsets, bad_unit=self.bad_unit[:n], scale=scale, bias=bias)
+                                   out_offsets=out_offsets, bad_unit=self.bad_unit[:n], scale=scale, bias=bias,
+                                   flags=l3.L3_DECODE_HINT_WIDE if wide else 0)
 
     def decode(self, src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor,
                out: torch.Tensor, *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0),
-               stream=None):
-        """Enqueue one batch decode on `stream`; returns (status, bad_unit) device views."""
-        a = self.args(src, src_offsets, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias)
+               stream=None, wide=False):
+        """Enqueue one batch decode on `stream`; returns (status, bad_unit) device views.
+        wide: performance hint for u8 batches of large images (policy N = 128), see l3.h."""
+        a = self.args(src, src_offsets, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide)
         l3.l3_decode_batch(a, stream)
         n = int(shapes.shape[0])
         return self.status[:n], self.bad_unit[:n]

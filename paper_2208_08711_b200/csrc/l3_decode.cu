@@ -32,6 +32,8 @@ struct ParseParams {
   int32_t* status;
   int32_t* bad_unit;
   WsView ws;
+  uint32_t tail_units;   // the last tail_units units of the batch run as 1-patch tasks (mode 4)
+  uint32_t wide;         // 1: 33 <= N <= 128 may use the wide 8-column path (u8 out); 0: always mode 4
 };
 
 __device__ __forceinline__ uint32_t ld_u32le(const uint8_t* p) {
@@ -76,52 +78,130 @@ __device__ void block_exclusive_scan2(uint64_t& a, uint64_t& b, uint64_t* sh_a, 
 
 // a1 for the whole batch by one thread block: validate each header (magic,
 // W/H/N, caller shape, offset-table size), build the per-image descriptor and
-// the exclusive task prefixes of the two decode classes (N <= 128, N > 128).
+// the exclusive task prefixes of the two decode classes (0: N <= 128, 1: N > 128).
 // The per-unit part of the offset check (strictly increasing, inside the data
 // section) is done by each unit when it is decoded.
-__device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
+// Tail zone: images whose units start within the batch's last `tail_units`
+// units (about one per resident warp) are decoded one patch per task on the
+// 4-column path (mode 4), so the end of the persistent kernel is fine-grained.
+__device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc& d) {
+  const uint64_t f0 = p.src_offsets[i], f1 = p.src_offsets[i + 1];
+  const uint64_t len = f1 > f0 ? f1 - f0 : 0;
+  const uint8_t* f = p.src + f0;
+  d = ImgDesc{};
+  const int32_t expH = p.shapes[2 * i], expW = p.shapes[2 * i + 1];
+  d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)expH * (uint64_t)expW;
+  if (f1 < f0 || len < 4 || __ldg(f) != 'L' || __ldg(f + 1) != '3' || __ldg(f + 2) != 'I' || __ldg(f + 3) != 'F')
+    return L3_E_UNRECOGNIZED_FORMAT;
+  if (len < 13) return L3_E_CORRUPT_HEADER;
+  d.W = ld_u32le(f + 4);
+  d.H = ld_u32le(f + 8);
+  d.N = __ldg(f + 12);
+  if (d.W == 0 || d.H == 0 || d.N == 0 || d.W != (uint32_t)expW || d.H != (uint32_t)expH) return L3_E_CORRUPT_HEADER;
+  const uint64_t gx = (d.W + d.N - 1) / d.N, gy = (d.H + d.N - 1) / d.N;
+  const uint64_t P = gx * gy;
+  const uint64_t hdr = 13ull + 12ull * P;
+  if (3ull * P >= (uint64_t)kMaxUnitsPerImage || len < hdr) return L3_E_CORRUPT_HEADER;
+  d.gx = (uint32_t)gx;
+  d.P = (uint32_t)P;
+  d.file_off = f0;
+  d.data_off = f0 + hdr;
+  d.data_len = len - hdr;
+  lanes_and_group(d.N, &d.L, &d.G, &d.mode);
+  return L3_OK;
+}
+
+// a1 without the tail zone (kernel variants without the wide path): one pass.
+__device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
   uint64_t carry0 = 0, carry1 = 0;
   for (int base = 0; base < p.n; base += blockDim.x) {
     const int i = base + threadIdx.x;
     uint64_t t0 = 0, t1 = 0;
     if (i < p.n) {
-      const uint64_t f0 = p.src_offsets[i], f1 = p.src_offsets[i + 1];
-      const uint64_t len = f1 > f0 ? f1 - f0 : 0;
-      const uint8_t* f = p.src + f0;
-      int st = L3_OK;
-      ImgDesc d = {};
-      const int32_t expH = p.shapes[2 * i], expW = p.shapes[2 * i + 1];
-      d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)expH * (uint64_t)expW;
-      if (f1 < f0 || len < 4 || __ldg(f) != 'L' || __ldg(f + 1) != '3' || __ldg(f + 2) != 'I' ||
-          __ldg(f + 3) != 'F') {
-        st = L3_E_UNRECOGNIZED_FORMAT;
-      } else if (len < 13) {
-        st = L3_E_CORRUPT_HEADER;
-      } else {
-        d.W = ld_u32le(f + 4);
-        d.H = ld_u32le(f + 8);
-        d.N = __ldg(f + 12);
-        if (d.W == 0 || d.H == 0 || d.N == 0 || d.W != (uint32_t)expW || d.H != (uint32_t)expH) {
-          st = L3_E_CORRUPT_HEADER;
-        } else {
-          const uint64_t gx = (d.W + d.N - 1) / d.N, gy = (d.H + d.N - 1) / d.N;
-          const uint64_t P = gx * gy;
-          const uint64_t hdr = 13ull + 12ull * P;
-          if (3ull * P >= (uint64_t)kMaxUnitsPerImage || len < hdr) {
-            st = L3_E_CORRUPT_HEADER;
-          } else {
-            d.gx = (uint32_t)gx;
-            d.P = (uint32_t)P;
-            d.file_off = f0;
-            d.data_off = f0 + hdr;
-            d.data_len = len - hdr;
-            lanes_and_group(d.N, &d.L, &d.G);
-            d.tasks = (uint32_t)((3ull * P + d.G - 1) / d.G);
-            if (d.N <= 128) t0 = d.tasks; else t1 = d.tasks;
-          }
+      ImgDesc d;
+      const int st = parse_header(p, i, d);
+      if (st == L3_OK) {
+        if (d.mode == 1 || d.mode == 2) {
+          d.mode = 4;
+          d.L = 32;
+          d.G = 1;
         }
+        d.tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
+        if (d.mode != 3) t0 = d.tasks; else t1 = d.tasks;
+      } else {
+        d.tasks = 0;
       }
-      if (st != L3_OK) d.tasks = 0;
+      p.ws.desc[i] = d;
+      p.ws.errkey[i] = kNoError;
+      p.status[i] = st;
+      if (p.bad_unit) p.bad_unit[i] = -1;
+    }
+    uint64_t tot0, tot1;
+    block_exclusive_scan2(t0, t1, sh_a, sh_b, tot0, tot1);
+    if (i < p.n) {
+      p.ws.prefix[0][i] = carry0 + t0;
+      p.ws.prefix[1][i] = carry1 + t1;
+    }
+    carry0 += tot0;
+    carry1 += tot1;
+  }
+  if (threadIdx.x == 0) {
+    p.ws.prefix[0][p.n] = carry0;
+    p.ws.prefix[1][p.n] = carry1;
+  }
+}
+
+template <bool WIDE>
+__device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
+  if (!WIDE) {   // every 33 <= N <= 128 image runs as 1-patch tasks (mode 4)
+    parse_phase_simple(p, sh_a, sh_b);
+    return;
+  }
+  // pass 1 (wide path only): total class-0 units, for the tail zone
+  uint64_t total_units = 0;
+  for (int base = 0; p.wide && base < p.n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    uint64_t u0 = 0, z = 0;
+    if (i < p.n) {
+      ImgDesc d;
+      if (parse_header(p, i, d) == L3_OK && d.mode != 3) u0 = 3ull * d.P;
+    }
+    uint64_t t0, t1;
+    block_exclusive_scan2(u0, z, sh_a, sh_b, t0, t1);
+    total_units += t0;
+  }
+  // pass 2: descriptors, modes, task prefixes (the descriptor is rebuilt after
+  // the units scan rather than held across it: this code shares the decode
+  // kernel's register budget)
+  uint64_t carry0 = 0, carry1 = 0, ucarry = 0;
+  for (int base = 0; base < p.n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    uint64_t units = 0, z = 0, ut = 0, zt;
+    if (p.wide) {   // uniform
+      if (i < p.n) {
+        ImgDesc d0;
+        if (parse_header(p, i, d0) == L3_OK && d0.mode != 3) units = 3ull * d0.P;
+      }
+      block_exclusive_scan2(units, z, sh_a, sh_b, ut, zt);
+    }
+    const uint64_t uex = units + ucarry;   // (exclusive) units of class 0 before image i
+    ucarry += ut;
+    uint64_t t0 = 0, t1 = 0;
+    if (i < p.n) {
+      ImgDesc d;
+      const int st = parse_header(p, i, d);
+      if (st == L3_OK) {
+        const uint64_t my_units = 3ull * d.P;
+        if (d.mode != 3 && d.mode != 0 && (!p.wide || uex + my_units + p.tail_units > total_units)) {
+          d.mode = 4;                      // one patch per task, 4-column lanes (fp32, or the tail zone)
+          d.L = 32;
+          d.G = 1;
+        }
+        d.tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
+        if (d.mode != 3) t0 = d.tasks; else t1 = d.tasks;
+      } else {
+        d.tasks = 0;
+      }
       p.ws.desc[i] = d;
       p.ws.errkey[i] = kNoError;
       p.status[i] = st;
@@ -145,7 +225,7 @@ __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b
 // Standalone a1 (l3_parse_batch): header validation and work decomposition only.
 __global__ void __launch_bounds__(1024) l3_parse_kernel(ParseParams p) {
   __shared__ uint64_t sh_a[33], sh_b[33];
-  parse_phase(p, sh_a, sh_b);
+  parse_phase<false>(p, sh_a, sh_b);
 }
 
 // ============================================================== a2-a7 helpers
@@ -388,13 +468,15 @@ cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
 
 // ============================================================== host launch
 static int g_sm_count = 0;
-static int g_occ[2] = {0, 0};
+static int g_occ[3] = {0, 0, 0};   // f32, u8 narrow, u8 wide
 
-template <bool F32>
+template <bool F32, bool WIDE>
 static int fused_occupancy() {
   int occ = 0;
-  cudaFuncSetAttribute(l3_decode_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem_bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32>, kWarpsPerCta * 32, fast_smem_bytes());
+  cudaFuncSetAttribute(l3_decode_kernel<F32, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fast_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32, WIDE>, kWarpsPerCta * 32,
+                                                fast_smem_bytes());
   return occ > 0 ? occ : 1;
 }
 
@@ -405,8 +487,9 @@ cudaError_t ensure_device_info() {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    g_occ[0] = fused_occupancy<false>();
-    g_occ[1] = fused_occupancy<true>();
+    g_occ[0] = fused_occupancy<true, false>();
+    g_occ[1] = fused_occupancy<false, false>();
+    g_occ[2] = fused_occupancy<false, true>();
   }
   return cudaSuccess;
 }
@@ -421,6 +504,8 @@ static ParseParams make_parse_params(const l3_decode_args* a) {
   pp.status = a->status;
   pp.bad_unit = a->bad_unit;
   pp.ws = WsView::at(a->workspace, a->n);
+  pp.tail_units = 0;
+  pp.wide = 0;
   return pp;
 }
 
@@ -442,9 +527,15 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   }
   dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
-  const int grid = g_sm_count * g_occ[f32 ? 1 : 0];
-  if (f32) l3_decode_kernel<true><<<grid, kWarpsPerCta * 32, fast_smem_bytes(), s>>>(dp);
-  else l3_decode_kernel<false><<<grid, kWarpsPerCta * 32, fast_smem_bytes(), s>>>(dp);
+  const bool wide = !f32 && (a->flags & L3_DECODE_HINT_WIDE);
+  const int variant = f32 ? 0 : (wide ? 2 : 1);
+  const int grid = g_sm_count * g_occ[variant];
+  dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
+  dp.pp.wide = wide ? 1u : 0u;
+  const size_t smem = fast_smem_bytes();
+  if (variant == 0) l3_decode_kernel<true, false><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
+  else if (variant == 1) l3_decode_kernel<false, false><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
+  else l3_decode_kernel<false, true><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@
 
 namespace l3 {
 
-constexpr int kRingPitch = kRingBytes + 16;   // ring + 16-byte wrap mirror
+constexpr int kRingPitch = kRingBytes + 64;   // per-warp ring region (+ wrap mirrors)
 
 __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -308,8 +308,18 @@ __device__ __noinline__ int unit_first_error(const uint8_t* src, uint64_t start,
   return L3_OK;
 }
 
-template <bool F32>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+}  // namespace l3
+
+#include "l3_decode_wide8.cuh"
+
+namespace l3 {
+
+// Variants (measured): without the wide 8-column path the kernel
+// fits 80 registers = 6 CTAs / 24 warps per SM (fp32 out, and u8 batches of
+// small patches); WIDE (u8 out, L3_DECODE_HINT_WIDE) carries the 8-column path
+// for 33 <= N <= 128 and runs at 4 CTAs per SM.
+template <bool F32, bool WIDE>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t sh_a[33], sh_b[33];
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   // publishes the work decomposition; the other CTAs wait on the ready flag
   // (CTA 0 is dispatched first, so the wait cannot starve it).
   if (blockIdx.x == 0) {
-    parse_phase(p.pp, sh_a, sh_b);
+    parse_phase<WIDE>(p.pp, sh_a, sh_b);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
@@ -361,8 +371,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     uint64_t next = 0;
     if (lane == 0) next = atomicAdd(&head->next_task[0], 1ull);
 
+    if (WIDE && (d.mode == 1 || d.mode == 2)) {   // u8 out, 33 <= N <= 128: wide 8-column lanes
+      phase_bits = (d.mode == 1) ? decode_task8<F32, 4>(p, d, img, t, ring, bars, phase_bits, lim, K)
+                                 : decode_task8<F32, 2>(p, d, img, t, ring, bars, phase_bits, lim, K);
+      task = __shfl_sync(0xffffffffu, next, 0);
+      continue;
+    }
+    // mode 0 (N <= 32): G >= 4 short patches per warp, each staged whole;
+    // mode 4 (33 <= N <= 128 with fp32 out, or the u8 tail zone): one patch per
+    // warp, 4 columns per lane, streamed
     const uint32_t G = d.G;
-    const bool stream = (G == 1);
+    const bool stream = (G == 1);   // mode 4 (G == 1) vs mode 0 (G >= 4)
     const uint32_t Lw = stream ? 32u : d.L;            // G == 1: the unit spans the warp
     const uint32_t seg = stream ? 0u : lane / Lw, j = stream ? (uint32_t)lane : lane % Lw;
     const uint32_t nunits = 3u * d.P;

@@ -33,6 +33,9 @@ struct ImgDesc {
   uint32_t G;          // units (patches) per warp task
   uint32_t L;          // lanes per unit (segment width, power of two)
   uint32_t tasks;      // ceil(3P / G)
+  uint32_t mode;       // decode path: 0 whole-staged 4-column lanes (N <= 32), 1 / 2 wide 8-column
+                       // lanes with 4 KB / 2 KB segment rings (65..128 / 33..64), 3 generic (N > 128)
+  uint32_t pad_;
 };
 
 // Workspace layout (256-byte aligned sections).
@@ -69,20 +72,28 @@ struct WsView {
   }
 };
 
-// Lanes per unit and units per task for patch size N:
-// 4 columns per lane, segment = next power of two >= ceil(N/4) lanes (N <= 128);
-// N > 128 uses a full warp with two 128-column chunks per lane. G is capped so a
-// whole task (G worst-case patches + alignment slack) fits the 8 KB ring; G = 1
-// tasks stream through the ring instead.
-__host__ __device__ inline void lanes_and_group(uint32_t N, uint32_t* L, uint32_t* G) {
+// Decode path, lanes per unit and units per task for patch size N:
+//  * N <= 32: 4 columns per lane, segment = next power of two >= ceil(N/4)
+//    lanes, G = 32 / L units per warp, capped so G worst-case patches (+ slack)
+//    fit the warp's 8 KB ring (the whole task is staged at once): mode 0;
+//  * 33..64: 8 columns per lane, L = 8, G = 4 units, each streamed through its
+//    own 2 KB ring: mode 2;
+//  * 65..128: 8 columns per lane, L = 16, G = 2 units, 4 KB rings: mode 1;
+//  * N > 128 (never chosen by the policy): generic path, one unit per warp,
+//    two 128-column chunks per lane: mode 3.
+__host__ __device__ inline void lanes_and_group(uint32_t N, uint32_t* L, uint32_t* G, uint32_t* mode) {
+  if (N > 128) { *L = 32; *G = 1; *mode = 3; return; }
+  if (N > 64) { *L = 16; *G = 2; *mode = 1; return; }
+  if (N > 32) { *L = 8; *G = 4; *mode = 2; return; }
   uint32_t need = (N + 3) / 4;
   uint32_t l = 1;
   while (l < need && l < 32) l <<= 1;
   uint32_t g = 32 / l;
   uint64_t worst = ((uint64_t)N * (12 + 8ull * N) + 7) / 8;   // all rows k = 8
-  while (g > 1 && g * worst + 32 > (uint64_t)kRingBytes) g >>= 1;
+  while (g > 1 && g * (worst + 48) > (uint64_t)kRingBytes) g >>= 1;
   *L = l;
   *G = g;
+  *mode = 0;
 }
 
 // ---------------------------------------------------------------- PTX helpers

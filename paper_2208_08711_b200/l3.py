@@ -17,7 +17,7 @@ import threading
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libl3_b200.so")
+LIB_PATH = os.environ.get("L3_B200_LIB_OVERRIDE") or os.path.join(_PKG, "libl3_b200.so")   # override: dev A/B only
 
 L3_OK, L3_E_INVALID_ARGUMENT, L3_E_UNRECOGNIZED_FORMAT, L3_E_CORRUPT_HEADER, L3_E_CORRUPT_STREAM, \
     L3_E_TRUNCATED_STREAM, L3_E_CUDA = range(7)
@@ -44,7 +44,12 @@ class l3_decode_args(ctypes.Structure):
         ("bad_unit", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_uint64),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
+
+
+L3_DECODE_HINT_WIDE = 1
 
 
 class l3_encode_args(ctypes.Structure):
@@ -131,7 +136,7 @@ def _stream(stream) -> int:
 
 
 def make_decode_args(src, src_offsets, shapes, out, status, workspace, *, out_offsets=None, bad_unit=None,
-                     scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0)) -> l3_decode_args:
+                     scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), flags=0) -> l3_decode_args:
     a = l3_decode_args()
     a.src = _dev_ptr(src, "src", torch.uint8)
     a.src_offsets = _dev_ptr(src_offsets, "src_offsets", torch.int64)
@@ -151,6 +156,7 @@ def make_decode_args(src, src_offsets, shapes, out, status, workspace, *, out_of
     a.bad_unit = _dev_ptr(bad_unit, "bad_unit", torch.int32)
     a.workspace = _dev_ptr(workspace, "workspace")
     a.workspace_bytes = workspace.numel() * workspace.element_size()
+    a.flags = int(flags)
     return a
 
 

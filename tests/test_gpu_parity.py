@@ -22,7 +22,7 @@ from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD  # noqa: E402
 F32_TOL = 1e-6
 
 
-def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), canary=True, gap=0):
+def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), canary=True, gap=0, wide=False):
     """Decode files on the GPU into per-image blocks (optionally separated by `gap` canary
     elements). Returns (list of arrays [3,H,W], status, bad_unit, flat output)."""
     src, offs = pack_files(files)
@@ -36,7 +36,8 @@ def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0)
     out = torch.full((total,), fill, dtype=dtype, device="cuda")
     dec = BatchDecoder(max(n, 1))
     sh = torch.tensor(np.array(shapes, np.int32).reshape(n, 2), device="cuda")
-    st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(out_off).cuda(), scale=scale, bias=bias)
+    st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(out_off).cuda(), scale=scale, bias=bias,
+                         wide=wide)
     torch.cuda.synchronize()
     flat = out.cpu().numpy()
     imgs = [flat[int(o):int(o) + s].reshape(3, h, w) for o, s, (h, w) in zip(out_off, sizes, shapes)]
@@ -44,8 +45,14 @@ def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0)
 
 
 def check_u8(imgs_ref, files, gap=7):
+    """u8 parity through both u8 kernel variants (narrow and L3_DECODE_HINT_WIDE)."""
+    for wide in (False, True):
+        _check_u8(imgs_ref, files, gap, wide)
+
+
+def _check_u8(imgs_ref, files, gap, wide):
     shapes = [im.shape[1:] for im in imgs_ref]
-    got, st, bad, flat, out_off, sizes = gpu_decode(files, shapes, gap=gap)
+    got, st, bad, flat, out_off, sizes = gpu_decode(files, shapes, gap=gap, wide=wide)
     assert st.tolist() == [0] * len(files), st
     for i, (g, r) in enumerate(zip(got, imgs_ref)):
         if not np.array_equal(g, r):
@@ -117,13 +124,19 @@ def test_config3_cityscapes_full_fp32_and_u8():
     dec = BatchDecoder(n)
     sh = torch.tensor([[1024, 2048]] * n, dtype=torch.int32, device="cuda")
     out = torch.empty((n, 3, 1024, 2048), dtype=torch.uint8, device="cuda")
-    st, _ = dec.decode(src, offs, sh, out)
-    torch.cuda.synchronize()
-    assert st.cpu().tolist() == [0] * n
-    got = out.cpu().numpy()
+    refs = []
     for i in range(n):
         st_o, _, ref, _ = l3ref.decode(files[i])
-        assert st_o == 0 and np.array_equal(got[i], ref), i
+        assert st_o == 0
+        refs.append(ref)
+    for wide in (False, True):
+        out.fill_(0xA5)
+        st, _ = dec.decode(src, offs, sh, out, wide=wide)
+        torch.cuda.synchronize()
+        assert st.cpu().tolist() == [0] * n
+        got = out.cpu().numpy()
+        for i in range(n):
+            assert np.array_equal(got[i], refs[i]), (wide, i)
     scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD)
     outf = torch.empty((n, 3, 1024, 2048), dtype=torch.float32, device="cuda")
     st, _ = dec.decode(src, offs, sh, outf, scale=scale, bias=bias)
@@ -193,10 +206,11 @@ def test_fault_injection_status_parity(seed):
     P = (-(-W // N)) * (-(-H // N))
     files = _corrupt_variants(rng, f, P) + [f]
     shapes = [(H, W)] * len(files)
-    _, st, bad, _, _, _ = gpu_decode(files, shapes)
-    for i, fi in enumerate(files):
-        rst, rbad, _, _ = l3ref.decode(fi, exp_shape=(H, W))
-        assert (st[i], bad[i]) == (rst, rbad), (i, st[i], bad[i], rst, rbad)
+    for dtype, wide in ((torch.uint8, False), (torch.uint8, True), (torch.float32, False)):
+        _, st, bad, _, _, _ = gpu_decode(files, shapes, dtype=dtype, wide=wide)
+        for i, fi in enumerate(files):
+            rst, rbad, _, _ = l3ref.decode(fi, exp_shape=(H, W))
+            assert (st[i], bad[i]) == (rst, rbad), (dtype, wide, i, st[i], bad[i], rst, rbad)
 
 
 def test_shape_mismatch_is_corrupt_header():
