@@ -1,5 +1,5 @@
 #!/bin/bash
-# One gpurun session: bench lines for every config + ncu launch list + one full ncu capture.
+# One gpurun session: bench lines for every config + ncu launch list + full ncu captures.
 set -x
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
@@ -8,10 +8,15 @@ timeout 600 python bench.py > gpurun_out/${TAG}_bench_c3_f32.json 2> gpurun_out/
 timeout 600 python bench.py --out u8 --no-cpu-baseline > gpurun_out/${TAG}_bench_c3_u8.json 2> gpurun_out/${TAG}_bench_c3_u8.err
 timeout 600 python bench.py --config c4_uhd --no-cpu-baseline > gpurun_out/${TAG}_bench_c4_u8.json 2> gpurun_out/${TAG}_bench_c4_u8.err
 timeout 600 python bench.py --config c2_imagenet --no-cpu-baseline > gpurun_out/${TAG}_bench_c2_u8.json 2> gpurun_out/${TAG}_bench_c2_u8.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/${TAG}_bench_reference.json 2> gpurun_out/${TAG}_bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_c3_f32.csv \
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:l3_decode_kernel -s 3 -c 1 \
   -o gpurun_out/${TAG}_prof_c3_f32 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:l3_decode_kernel -s 3 -c 1 \
   -o gpurun_out/${TAG}_prof_c3_u8 -f python bench.py --out u8 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full_u8.log 2>&1
-ls -la gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:l3_decode_kernel -s 3 -c 1 \
+  -o gpurun_out/${TAG}_prof_c4_u8 -f python bench.py --config c4_uhd --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:l3_decode_kernel -s 3 -c 1 \
+  -o gpurun_out/${TAG}_prof_c2_u8 -f python bench.py --config c2_imagenet --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full_c2.log 2>&1
+ls -la gpurun_out | grep ${TAG}

@@ -84,15 +84,21 @@ if __name__ == "__main__":
     tag, gp = sys.argv[1], sys.argv[2]   # e.g. r1 gpurun_out/r1b
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
-    samples = 32 * 3 * 2048 * 1024
-    for out_kind in ("f32", "u8"):
-        rep = f"{gp}_prof_c3_{out_kind}.ncu-rep"
+    sys.path.insert(0, ROOT)
+    import l3synth
+    c2 = sum(3 * h * w for h, w in l3synth.imagenet_shapes(256))
+    cases = {"c3_f32": ("c3_cityscapes_f32", 32 * 3 * 2048 * 1024, "C3 Cityscapes 32x2048x1024, fp32 out"),
+             "c3_u8": ("c3_cityscapes_u8", 32 * 3 * 2048 * 1024, "C3 Cityscapes 32x2048x1024, u8 out"),
+             "c4_u8": ("c4_uhd_u8", 16 * 3 * 3840 * 2160, "C4 UHD 16x3840x2160, u8 out (wide variant)"),
+             "c2_u8": ("c2_imagenet_u8", c2, "C2 ImageNet-shaped 256 x ~500x375, u8 out")}
+    for key, (tkey, samples, title) in cases.items():
+        rep = f"{gp}_prof_{key}.ncu-rep"
         if not os.path.exists(rep):
             continue
         md, t = kernel_md(rep, samples)
-        traffic[f"c3_cityscapes_{out_kind}"] = t
-        with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_c3_{out_kind}.md"), "w") as f:
-            f.write(f"# {tag}: ncu --set full, decode kernel, C3 Cityscapes 32x2048x1024, out={out_kind}\n\n")
+        traffic[tkey] = t
+        with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{key}.md"), "w") as f:
+            f.write(f"# {tag}: ncu --set full, decode kernel, {title}\n\n")
             f.write(f"Source: `{os.path.basename(rep)}` (one launch, `-s 3 -c 1`, --clock-control none).\n\n")
             f.write(md)
     lc = f"{gp}_launches_c3_f32.csv"
