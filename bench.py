@@ -44,6 +44,10 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for the barrier / max-over-ranks plumbing (gloo: single-GPU tests)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="all ranks on cuda:0 (multi-rank plumbing tests on a 1-GPU box; not a scaling run)")
     return ap.parse_args()
 
 
@@ -203,10 +207,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev_index = 0 if args.share_device else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     out_kind = args.out or ("f32" if args.config == "c3_cityscapes" else "u8")
     out_dtype = torch.float32 if out_kind == "f32" else torch.uint8
 
@@ -260,7 +268,7 @@ def main():
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev_index)
     torch.cuda.synchronize()
     with sampler:
         t_start.record(stream)

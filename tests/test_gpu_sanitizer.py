@@ -1,0 +1,27 @@
+"""compute-sanitizer over every decode mode, both u8 variants, fp32 and the error paths
+(SURVEY.md §4 item 5): no memory errors, no shared-memory races, no uninitialised reads."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "scripts", "sanitize_case.py")], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "0 errors" in out or "0 hazards" in out, out[-2000:]
+    # the truncated file and the k = 0 file must be reported
+    assert "5, 4]" in out or "5, 4" in out, out[-2000:]
