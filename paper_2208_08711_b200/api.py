@@ -115,3 +115,53 @@ def encode_batch(images: Sequence[np.ndarray] | Sequence[torch.Tensor], patch_si
     src = torch.empty(max(total, 1), dtype=torch.uint8, device=device)
     src[:total].copy_(dst[:total])
     return src, dst_offsets
+
+
+class PipelinedLoader:
+    """Load + decode pipeline (SURVEY.md §8(f1); PAPER.md:67 Load stage, :189 "we allocate both
+    processes to separate CUDA streams. We prioritize the computing stream over the decoding
+    stream"). Batch i+1's compressed bytes move host -> HBM on a copy stream while batch i decodes
+    on a decode stream; both streams get the LOWEST priority so a training step on a
+    high-priority compute stream is not delayed by them. Double-buffered device staging.
+
+    submit() enqueues one batch (pinned host bytes) and returns the (status, out) it will fill;
+    the host copy of the statuses of batch i is readable after `wait(i)`."""
+
+    def __init__(self, max_n: int, max_bytes: int, depth: int = 2, device="cuda"):
+        lo, _hi = torch.cuda.Stream.priority_range()
+        self.device = torch.device(device)
+        self.copy_stream = torch.cuda.Stream(device=self.device, priority=lo)
+        self.decode_stream = torch.cuda.Stream(device=self.device, priority=lo)
+        self.stage = [torch.empty(max_bytes + 16, dtype=torch.uint8, device=self.device) for _ in range(depth)]
+        self.dec = [BatchDecoder(max_n, self.device) for _ in range(depth)]
+        self.copied = [torch.cuda.Event() for _ in range(depth)]
+        self.freed = [torch.cuda.Event() for _ in range(depth)]
+        self.host_status = [torch.empty(max_n, dtype=torch.int32).pin_memory() for _ in range(depth)]
+        self.done = [torch.cuda.Event() for _ in range(depth)]
+        self.i = 0
+
+    def submit(self, host_src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor, out: torch.Tensor,
+               *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), wide=False) -> int:
+        b = self.i % len(self.stage)
+        nbytes = host_src.numel()
+        with torch.cuda.stream(self.copy_stream):
+            if self.i >= len(self.stage):
+                self.copy_stream.wait_event(self.freed[b])          # staging buffer b no longer read
+            self.stage[b][:nbytes].copy_(host_src, non_blocking=True)
+            self.copied[b].record(self.copy_stream)
+        self.decode_stream.wait_event(self.copied[b])
+        n = int(shapes.shape[0])
+        a = self.dec[b].args(self.stage[b], src_offsets, shapes, out, out_offsets=out_offsets, scale=scale,
+                             bias=bias, wide=wide)
+        l3.l3_decode_batch(a, self.decode_stream)
+        self.freed[b].record(self.decode_stream)
+        with torch.cuda.stream(self.decode_stream):
+            self.host_status[b][:n].copy_(self.dec[b].status[:n], non_blocking=True)
+        self.done[b].record(self.decode_stream)
+        self.i += 1
+        return self.i - 1
+
+    def wait(self, ticket: int) -> torch.Tensor:
+        b = ticket % len(self.stage)
+        self.done[b].synchronize()
+        return self.host_status[b]
