@@ -79,6 +79,12 @@ typedef void* l3_stream_t;
  *   workspace    device, >= l3_decode_workspace_size(n) bytes, 256-byte aligned,
  *                zero-filled before first use (see l3_decode_batch).
  *   flags        L3_DECODE_HINT_* performance hints (0 = none).
+ *   crops        optional: image i is decoded only inside the window rows [y, y+h) x cols
+ *                [x, x+w) (flip != 0: mirrored left-right) into a [3, h, w] block (dense:
+ *                element i*3*h*w). Only the patches the window touches are read and decoded
+ *                (patches are independently addressable); status then covers
+ *                the header and those patches. A window outside the image is
+ *                L3_E_INVALID_ARGUMENT in status[i].
  */
 /* l3_decode_args.flags */
 #define L3_DECODE_HINT_WIDE 1u   /* u8 out: most files use 33 <= N <= 128 (e.g. policy N = 128 for
@@ -101,6 +107,7 @@ typedef struct {
   uint64_t workspace_bytes;
   uint32_t flags;   /* L3_DECODE_HINT_* bits, 0 = none */
   uint32_t reserved;
+  const int32_t* crops;   /* device, n x {y, x, h, w, flip} or NULL (partial decode) */
 } l3_decode_args;
 
 /* Bytes of device workspace one l3_decode_batch call over n images needs. */

@@ -28,6 +28,7 @@ struct ParseParams {
   const uint64_t* src_offsets;
   const int32_t* shapes;
   const uint64_t* out_offsets;
+  const int32_t* crops;  // n x {y, x, h, w, flip} or NULL (f3: partial decode)
   int32_t n;
   int32_t* status;
   int32_t* bad_unit;
@@ -90,7 +91,22 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
   const uint8_t* f = p.src + f0;
   d = ImgDesc{};
   const int32_t expH = p.shapes[2 * i], expW = p.shapes[2 * i + 1];
-  d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)expH * (uint64_t)expW;
+  int32_t cy = 0, cx = 0, chh = expH, cww = expW, flip = 0;
+  if (p.crops) {
+    cy = p.crops[5 * i];
+    cx = p.crops[5 * i + 1];
+    chh = p.crops[5 * i + 2];
+    cww = p.crops[5 * i + 3];
+    flip = p.crops[5 * i + 4];
+  }
+  d.cy = (uint32_t)cy;
+  d.cx = (uint32_t)cx;
+  d.ch = (uint32_t)chh;
+  d.cw = (uint32_t)cww;
+  d.flip = flip ? 1u : 0u;
+  d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)(uint32_t)chh * (uint32_t)cww;
+  if (p.crops && (cy < 0 || cx < 0 || chh < 1 || cww < 1 || (int64_t)cy + chh > expH || (int64_t)cx + cww > expW))
+    return L3_E_INVALID_ARGUMENT;
   if (f1 < f0 || len < 4 || __ldg(f) != 'L' || __ldg(f + 1) != '3' || __ldg(f + 2) != 'I' || __ldg(f + 3) != 'F')
     return L3_E_UNRECOGNIZED_FORMAT;
   if (len < 13) return L3_E_CORRUPT_HEADER;
@@ -268,34 +284,54 @@ __device__ __forceinline__ void stage_range(const uint8_t* src, uint64_t a16, ui
 // but is a valid file; these tasks run after all N <= 128 tasks inside the same
 // persistent kernel. Stream-staged through the warp's ring like the fast path
 // (G = 1), but reading with an explicit byte swap (no pre-swap, no mirror).
-template <bool F32>
-__device__ __noinline__ uint32_t generic_task(const DecodeParams& p, uint64_t task, uint8_t* ring8, uint64_t* bars,
+// Arguments of the generic path as plain values: passing the kernel's parameter
+// struct by reference to a non-inlined function makes the compiler keep the
+// whole struct in local memory and read hot-path fields from there (LDL on
+// every task; measured 8 % slower, profiles/r1 notes).
+struct GenericArgs {
+  const uint8_t* src;
+  const uint64_t* prefix1;
+  const ImgDesc* desc;
+  uint32_t* errkey;
+  void* out;
+  uint64_t lim;
+  int n;
+  float scale[3], bias[3];
+};
+
+template <bool F32, bool CROP>
+__device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uint8_t* ring8, uint64_t* bars,
                                               uint32_t phase_bits) {
   constexpr int MAXCH = 2;
   const int lane = threadIdx.x & 31;
   const uint32_t* ring = reinterpret_cast<const uint32_t*>(ring8);
-  const uint64_t* prefix = p.pp.ws.prefix[1];
-  const uint64_t lim = p.pp.src_offsets[p.pp.n] & ~15ull;
-  int lo = 0, hi = p.pp.n;
+  const uint64_t* prefix = ga.prefix1;
+  const uint64_t lim = ga.lim;
+  int lo = 0, hi = ga.n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
   }
   const int img = lo;
-  const ImgDesc d = p.pp.ws.desc[img];
+  const ImgDesc d = ga.desc[img];
   const uint32_t u = (uint32_t)(task - prefix[img]);   // G = 1: task = unit
   const uint32_t j = lane;
   const uint32_t nunits = 3u * d.P;
-  const uint8_t* file = p.pp.src + d.file_off;
+  const uint8_t* file = ga.src + d.file_off;
 
   const uint32_t ch = u / d.P;
   const uint32_t pp = u - ch * d.P;
   const uint32_t x0 = (pp % d.gx) * d.N, y0 = (pp / d.gx) * d.N;
-  const uint32_t w = min(d.N, d.W - x0), h = min(d.N, d.H - y0);
+  const uint32_t w = min(d.N, d.W - x0);
+  uint32_t h = min(d.N, d.H - y0);
+  if (CROP) {   // f3: skip patches outside the window; rows below it are not needed
+    if (x0 + w <= d.cx || x0 >= d.cx + d.cw || y0 + h <= d.cy || y0 >= d.cy + d.ch) return phase_bits;
+    h = min(h, d.cy + d.ch - y0);
+  }
   const uint64_t off = ld_u32le(file + 13 + 4ull * u);
   const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
   if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
-    if (lane == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+    if (lane == 0) atomicMin(&ga.errkey[img], 0u);   // header-level: CORRUPT_HEADER
     return phase_bits;
   }
   const uint64_t start = d.data_off + off, end = d.data_off + nxt;
@@ -311,14 +347,14 @@ __device__ __noinline__ uint32_t generic_task(const DecodeParams& p, uint64_t ta
   uint32_t issued = min(nchunks, (uint32_t)kSlots), landed = 0;
   for (uint32_t c = 0; c < issued; c++) {
     const uint64_t ca = A + (uint64_t)c * kSlotBytes;
-    stage_range(p.pp.src, ca, min(ca + kSlotBytes, B), lim, stage_end, ring8 + c * kSlotBytes, &bars[c],
+    stage_range(ga.src, ca, min(ca + kSlotBytes, B), lim, stage_end, ring8 + c * kSlotBytes, &bars[c],
                 lane == 0, lane, 32);
   }
   __syncwarp();
   const uint32_t seg_bit0 = bitpos;
-  const uint64_t plane = d.out_off + (uint64_t)ch * d.W * d.H;
-  const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
-  const float bi = F32 ? (ch == 0 ? p.bias[0] : (ch == 1 ? p.bias[1] : p.bias[2])) : 0.f;
+  const uint64_t plane = CROP ? d.out_off + (uint64_t)ch * d.ch * d.cw : d.out_off + (uint64_t)ch * d.W * d.H;
+  const float sc = F32 ? (ch == 0 ? ga.scale[0] : (ch == 1 ? ga.scale[1] : ga.scale[2])) : 0.f;
+  const float bi = F32 ? (ch == 0 ? ga.bias[0] : (ch == 1 ? ga.bias[1] : ga.bias[2])) : 0.f;
   int prev[MAXCH][4];
 #pragma unroll
   for (int q = 0; q < MAXCH; q++)
@@ -347,7 +383,7 @@ __device__ __noinline__ uint32_t generic_task(const DecodeParams& p, uint64_t ta
       else if (k == 0 || k > 8) code = L3_E_CORRUPT_STREAM;
       else if (avail < 12u + k * w) code = L3_E_TRUNCATED_STREAM;
       if (code != L3_OK) {
-        if (lane == 0) atomicMin(&p.pp.ws.errkey[img], err_key(u, code));
+        if (lane == 0) atomicMin(&ga.errkey[img], err_key(u, code));
         dead = true;
         live = false;
         k = 1;
@@ -396,17 +432,24 @@ __device__ __noinline__ uint32_t generic_task(const DecodeParams& p, uint64_t ta
     }
     // a6: store
     if (live) {
-      const uint64_t row_off = plane + (uint64_t)(y0 + r) * d.W + x0;
+      const int32_t ri = (int32_t)(y0 + r) - (int32_t)d.cy;
+      const bool row_in = !CROP || (uint32_t)ri < d.ch;
+      const uint64_t row_off = CROP ? plane + (uint64_t)(uint32_t)ri * d.cw : plane + (uint64_t)(y0 + r) * d.W + x0;
 #pragma unroll
       for (int q = 0; q < MAXCH; q++) {
         const uint32_t c = q * 128u + 4u * j;
-        if (c >= w) continue;
-        const uint64_t e = row_off + c;
+        if (c >= w || !row_in) continue;
 #pragma unroll
         for (int s = 0; s < 4; s++) {
           if (c + s >= w) break;
-          if (F32) reinterpret_cast<float*>(p.out)[e + s] = fmaf((float)pix[q][s], sc, bi);
-          else reinterpret_cast<uint8_t*>(p.out)[e + s] = (uint8_t)pix[q][s];
+          uint64_t e = row_off + c + s;
+          if (CROP) {
+            const int32_t cj = (int32_t)(x0 + c + s) - (int32_t)d.cx;
+            if ((uint32_t)cj >= d.cw) continue;
+            e = row_off + (d.flip ? d.cw - 1u - (uint32_t)cj : (uint32_t)cj);
+          }
+          if (F32) reinterpret_cast<float*>(ga.out)[e] = fmaf((float)pix[q][s], sc, bi);
+          else reinterpret_cast<uint8_t*>(ga.out)[e] = (uint8_t)pix[q][s];
         }
       }
 #pragma unroll
@@ -422,7 +465,7 @@ __device__ __noinline__ uint32_t generic_task(const DecodeParams& p, uint64_t ta
       fence_proxy_async_smem();
       while (issued < nchunks && issued < consumed + kSlots) {
         const uint64_t ca = A + (uint64_t)issued * kSlotBytes;
-        stage_range(p.pp.src, ca, min(ca + kSlotBytes, B), lim, stage_end,
+        stage_range(ga.src, ca, min(ca + kSlotBytes, B), lim, stage_end,
                     ring8 + (issued % kSlots) * kSlotBytes, &bars[issued % kSlots], lane == 0, lane, 32);
         issued++;
       }
@@ -468,14 +511,14 @@ cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
 
 // ============================================================== host launch
 static int g_sm_count = 0;
-static int g_occ[3] = {0, 0, 0};   // f32, u8 narrow, u8 wide
+static int g_occ[5] = {0, 0, 0, 0, 0};   // f32, u8 narrow, u8 wide, f32 crop, u8 crop
 
-template <bool F32, bool WIDE>
+template <bool F32, bool WIDE, bool CROP>
 static int fused_occupancy() {
   int occ = 0;
-  cudaFuncSetAttribute(l3_decode_kernel<F32, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(l3_decode_kernel<F32, WIDE, CROP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)fast_smem_bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32, WIDE>, kWarpsPerCta * 32,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32, WIDE, CROP>, kWarpsPerCta * 32,
                                                 fast_smem_bytes());
   return occ > 0 ? occ : 1;
 }
@@ -487,9 +530,11 @@ cudaError_t ensure_device_info() {
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    g_occ[0] = fused_occupancy<true, false>();
-    g_occ[1] = fused_occupancy<false, false>();
-    g_occ[2] = fused_occupancy<false, true>();
+    g_occ[0] = fused_occupancy<true, false, false>();
+    g_occ[1] = fused_occupancy<false, false, false>();
+    g_occ[2] = fused_occupancy<false, true, false>();
+    g_occ[3] = fused_occupancy<true, false, true>();
+    g_occ[4] = fused_occupancy<false, false, true>();
   }
   return cudaSuccess;
 }
@@ -500,6 +545,7 @@ static ParseParams make_parse_params(const l3_decode_args* a) {
   pp.src_offsets = a->src_offsets;
   pp.shapes = a->shapes;
   pp.out_offsets = a->out_offsets;
+  pp.crops = a->crops;
   pp.n = a->n;
   pp.status = a->status;
   pp.bad_unit = a->bad_unit;
@@ -527,15 +573,21 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   }
   dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
-  const bool wide = !f32 && (a->flags & L3_DECODE_HINT_WIDE);
-  const int variant = f32 ? 0 : (wide ? 2 : 1);
+  const bool crop = a->crops != nullptr;
+  const bool wide = !f32 && !crop && (a->flags & L3_DECODE_HINT_WIDE);
+  const int variant = crop ? (f32 ? 3 : 4) : (f32 ? 0 : (wide ? 2 : 1));
   const int grid = g_sm_count * g_occ[variant];
   dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
   dp.pp.wide = wide ? 1u : 0u;
   const size_t smem = fast_smem_bytes();
-  if (variant == 0) l3_decode_kernel<true, false><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
-  else if (variant == 1) l3_decode_kernel<false, false><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
-  else l3_decode_kernel<false, true><<<grid, kWarpsPerCta * 32, smem, s>>>(dp);
+  const dim3 B(kWarpsPerCta * 32);
+  switch (variant) {
+    case 0: l3_decode_kernel<true, false, false><<<grid, B, smem, s>>>(dp); break;
+    case 1: l3_decode_kernel<false, false, false><<<grid, B, smem, s>>>(dp); break;
+    case 2: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
+    case 3: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
+    default: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
+  }
   return cudaGetLastError();
 }
 

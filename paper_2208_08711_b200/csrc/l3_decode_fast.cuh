@@ -168,6 +168,11 @@ struct LaneRows {
   uint8_t* optr;      // output of column j4 in the current row
   uint32_t pitch;     // bytes between output rows
   uint32_t A, B;      // previous row, pair form: A = (c0, c1), B = (c2, c3)
+  // CROP variant only (f3, partial decode): output window mapping
+  int32_t ri;         // current image row - crop top
+  int32_t cj0;        // first column of this lane - crop left
+  uint32_t cw, chh;   // crop width / height
+  bool flip;          // horizontal flip of the window
 };
 
 template <bool F32, bool FAST>
@@ -203,6 +208,24 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
   }
 }
 
+// f3: store the lane's 4 samples into a cropped (optionally flipped) window.
+template <bool F32>
+__device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi,
+                                            bool pred) {
+  if (!pred || (uint32_t)s.ri >= s.chh) return;
+  const uint32_t x[4] = {xA & 0xFFFFu, xA >> 16, xB & 0xFFFFu, xB >> 16};
+  const uint64_t row = (uint64_t)(uint32_t)s.ri * s.cw;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int32_t c = s.cj0 + t;
+    if (s.j4 + t < s.w && (uint32_t)c < s.cw) {
+      const uint64_t e = row + (s.flip ? (s.cw - 1u - (uint32_t)c) : (uint32_t)c);
+      if (F32) reinterpret_cast<float*>(s.optr)[e] = fmaf((float)x[t], sc, bi);
+      else s.optr[e] = (uint8_t)x[t];
+    }
+  }
+}
+
 // One row of one lane (a3-a6). FIRST: row 0 of the patch (no prediction,
 // PAPER.md:139 "the first row is stored in a raw data format").
 // Validity is accumulated, not tested per row: kacc collects every row's k
@@ -211,7 +234,7 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
 // that case (reads stay inside the ring, writes inside the patch) and the
 // exact first error is re-derived after the patch (unit_first_error).
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
-template <bool FIRST, bool F32, bool FAST, bool GUARD>
+template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP>
 __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
   const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
@@ -254,7 +277,8 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
   }
   // a6: store (u8 planar, or fused cast + normalise)
-  store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
+  if (CROP) store4_crop<F32>(s, xA, xB, sc, bi, live && s.valid);
+  else store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
   s.A = xA;
   s.B = xB;
   if (live) {
@@ -262,10 +286,11 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     s.bp = nbp;
     s.raw = raw_next;
   }
-  s.optr += s.pitch;
+  if (CROP) s.ri++;
+  else s.optr += s.pitch;
 }
 
-template <bool F32, bool FAST, bool STREAM>
+template <bool F32, bool FAST, bool STREAM, bool CROP>
 __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uint32_t hmax, uint32_t Lw, float sc,
                                                  float bi, uint32_t K, const uint8_t* src, uint64_t lim,
                                                  StreamState& st, uint64_t* bars, uint32_t& phase_bits,
@@ -274,18 +299,18 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
     stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
   s.raw = rbits(ring, s.bp);
-  decode_row<true, F32, FAST, GUARD>(s, ring, 0, Lw, sc, bi, K);
+  decode_row<true, F32, FAST, GUARD, CROP>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
-    decode_row<false, F32, FAST, GUARD>(s, ring, r, Lw, sc, bi, K);
-    decode_row<false, F32, FAST, GUARD>(s, ring, r + 1, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
-    decode_row<false, F32, FAST, GUARD>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r, Lw, sc, bi, K);
   }
 }
 
@@ -318,7 +343,7 @@ namespace l3 {
 // fits 80 registers = 6 CTAs / 24 warps per SM (fp32 out, and u8 batches of
 // small patches); WIDE (u8 out, L3_DECODE_HINT_WIDE) carries the 8-column path
 // for 33 <= N <= 128 and runs at 4 CTAs per SM.
-template <bool F32, bool WIDE>
+template <bool F32, bool WIDE, bool CROP>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -399,6 +424,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
       y0 = py * d.N;
       w = min(d.N, d.W - x0);
       h = min(d.N, d.H - y0);
+      if (CROP) {   // f3: skip patches outside the window; rows below it are not needed
+        if (x0 + w <= d.cx || x0 >= d.cx + d.cw || y0 + h <= d.cy || y0 >= d.cy + d.ch) active = false;
+        else h = min(h, d.cy + d.ch - y0);
+      }
+    }
+    if (active) {
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
       if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
@@ -422,9 +453,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     s.kacc = 0;
     s.A = s.B = 0;
     const uint32_t esz = F32 ? 4u : 1u;
-    const uint64_t elem = d.out_off + (uint64_t)ch * d.W * d.H + (uint64_t)y0 * d.W + x0 + s.j4;
-    s.optr = reinterpret_cast<uint8_t*>(p.out) + elem * esz;
-    s.pitch = d.W * esz;
+    if (CROP) {
+      s.optr = reinterpret_cast<uint8_t*>(p.out) + (d.out_off + (uint64_t)ch * d.ch * d.cw) * esz;
+      s.pitch = 0;
+      s.ri = (int32_t)y0 - (int32_t)d.cy;
+      s.cj0 = (int32_t)(x0 + s.j4) - (int32_t)d.cx;
+      s.cw = d.cw;
+      s.chh = d.ch;
+      s.flip = d.flip != 0;
+    } else {
+      const uint64_t elem = d.out_off + (uint64_t)ch * d.W * d.H + (uint64_t)y0 * d.W + x0 + s.j4;
+      s.optr = reinterpret_cast<uint8_t*>(p.out) + elem * esz;
+      s.pitch = d.W * esz;
+    }
     const uint32_t len = active ? (uint32_t)min((uint64_t)(worst + 16), end - start) : 0u;
 
     StreamState st;
@@ -477,8 +518,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     uint32_t hmax = s.h;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
-    const bool fast_ok = !active || ((w & 3u) == 0 && ((reinterpret_cast<uintptr_t>(s.optr) & (F32 ? 15 : 3)) == 0) &&
-                                     ((s.pitch & (F32 ? 15u : 3u)) == 0));
+    const bool fast_ok = !active || ((w & 3u) == 0 && (CROP || (((reinterpret_cast<uintptr_t>(s.optr) &
+                                                                   (F32 ? 15 : 3)) == 0) &&
+                                                                 ((s.pitch & (F32 ? 15u : 3u)) == 0))));
     const bool fast = __all_sync(0xffffffffu, fast_ok);
     const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
     const float bi = F32 ? (ch == 0 ? p.bias[0] : (ch == 1 ? p.bias[1] : p.bias[2])) : 0.f;
@@ -486,14 +528,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     if (hmax > 0) {
       if (stream) {
         if (fast)
-          decode_unit_rows<F32, true, true>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, true, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, true>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, true, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       } else {
         if (fast)
-          decode_unit_rows<F32, true, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, false, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, false, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       }
     }
     const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
@@ -517,12 +559,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
   // ---- N > 128 units (never chosen by the policy): generic path, same ring
   const uint64_t total1 = p.pp.ws.prefix[1][p.pp.n];
   if (total1 > 0) {
+    GenericArgs ga;
+    ga.src = p.pp.src;
+    ga.prefix1 = p.pp.ws.prefix[1];
+    ga.desc = p.pp.ws.desc;
+    ga.errkey = p.pp.ws.errkey;
+    ga.out = p.out;
+    ga.lim = lim;
+    ga.n = p.pp.n;
+    for (int c = 0; c < 3; c++) {
+      ga.scale[c] = p.scale[c];
+      ga.bias[c] = p.bias[c];
+    }
     for (;;) {
       uint64_t t1 = 0;
       if (lane == 0) t1 = atomicAdd(&head->next_task[1], 1ull);
       t1 = __shfl_sync(0xffffffffu, t1, 0);
       if (t1 >= total1) break;
-      phase_bits = generic_task<F32>(p, t1, ring, bars, phase_bits);
+      phase_bits = generic_task<F32, CROP>(ga, t1, ring, bars, phase_bits);
     }
   }
 

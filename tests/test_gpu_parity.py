@@ -285,3 +285,88 @@ def test_pipelined_loader_matches_direct_decode():
         ref = imgs[:3] if k % 2 == 0 else imgs[3:]
         for i in range(3):
             assert np.array_equal(out[i].cpu().numpy(), ref[i])
+
+
+# ------------------------------------------------------------------ f3: partial decode (crop / flip)
+
+def _crop_decode(files, shapes, crops, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0)):
+    src, offs = pack_files(files)
+    n = len(files)
+    sizes = [3 * int(c[2]) * int(c[3]) for c in crops]
+    oo = np.zeros(n, np.int64)
+    oo[1:] = np.cumsum(sizes)[:-1]
+    fill = 0xA5 if dtype == torch.uint8 else float("nan")
+    out = torch.full((sum(sizes),), fill, dtype=dtype, device="cuda")
+    dec = BatchDecoder(n)
+    sh = torch.tensor(np.array(shapes, np.int32).reshape(n, 2), device="cuda")
+    cr = torch.tensor(np.array(crops, np.int32).reshape(n, 5), device="cuda")
+    st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(oo).cuda(), scale=scale, bias=bias,
+                         crops=cr)
+    torch.cuda.synchronize()
+    flat = out.cpu().numpy()
+    return [flat[int(o):int(o) + s].reshape(3, int(c[2]), int(c[3])) for o, s, c in zip(oo, sizes, crops)], \
+        st.cpu().numpy()
+
+
+def _window(img, c):
+    y, x, h, w, flip = c
+    v = img[:, y:y + h, x:x + w]
+    return v[:, :, ::-1] if flip else v
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_crop_flip_matches_oracle(seed):
+    rng = np.random.default_rng(seed)
+    imgs, files, crops = [], [], []
+    for i in range(10):
+        H, W = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+        N = int(rng.choice([0, 5, 16, 32, 64, 100, 128, 160, 255]))
+        im = l3synth.uniform_image(H, W, 50 * seed + i)
+        imgs.append(im)
+        files.append(l3ref.encode(im, N=N))
+        h = int(rng.integers(1, H + 1)); w = int(rng.integers(1, W + 1))
+        crops.append((int(rng.integers(0, H - h + 1)), int(rng.integers(0, W - w + 1)), h, w, int(rng.integers(0, 2))))
+    for dtype in (torch.uint8, torch.float32):
+        scale, bias = ((1, 1, 1), (0, 0, 0)) if dtype == torch.uint8 else normalize_constants(IMAGENET_MEAN,
+                                                                                              IMAGENET_STD)
+        got, st = _crop_decode(files, [im.shape[1:] for im in imgs], crops, dtype, scale, bias)
+        assert st.tolist() == [0] * len(files)
+        for g, im, c in zip(got, imgs, crops):
+            ref = _window(im, c)
+            if dtype == torch.uint8:
+                assert np.array_equal(g, ref), c
+            else:
+                assert np.abs(g.astype(np.float64) - l3ref.normalize(np.ascontiguousarray(ref), IMAGENET_MEAN,
+                                                                     IMAGENET_STD)).max() <= F32_TOL
+
+
+def test_crop_config3_random_crops():
+    """Cityscapes-shaped images, training-style random 512x1024 crops with flips."""
+    imgs = l3synth.make_batch("c3_cityscapes", 4)
+    files = [l3ref.encode(im) for im in imgs]
+    crops = [(100, 300, 512, 1024, 0), (0, 0, 512, 1024, 1), (511, 1023, 513, 1025, 1), (37, 901, 512, 1024, 0)]
+    got, st = _crop_decode(files, [im.shape[1:] for im in imgs], crops)
+    assert st.tolist() == [0] * 4
+    for g, im, c in zip(got, imgs, crops):
+        assert np.array_equal(g, _window(im, c))
+
+
+def test_crop_invalid_window_status():
+    im = l3synth.natural(40, 50, 1, 1.0)
+    f = l3ref.encode(im)
+    got, st = _crop_decode([f, f, f], [(40, 50)] * 3, [(0, 0, 40, 50, 0), (30, 0, 11, 50, 0), (0, -1, 4, 4, 0)])
+    assert st.tolist() == [0, 1, 1]
+    assert np.array_equal(got[0], im)
+
+
+def test_crop_skips_patches_outside_the_window():
+    """A corrupted patch outside the window is never read: the cropped decode stays OK (partial decode)."""
+    im = l3synth.natural(256, 256, 3, 1.0)
+    f = bytearray(l3ref.encode(im, N=64))
+    P = 16
+    offs = np.frombuffer(bytes(f[13:13 + 12 * P]), "<u4")
+    f[13 + 12 * P + int(offs[15])] &= 0x0F            # k = 0 in unit 15 (bottom-right patch of R)
+    got, st = _crop_decode([bytes(f)], [(256, 256)], [(0, 0, 64, 64, 0)])
+    assert st.tolist() == [0] and np.array_equal(got[0], im[:, :64, :64])
+    got, st = _crop_decode([bytes(f)], [(256, 256)], [(192, 192, 64, 64, 0)])
+    assert st.tolist() == [4]
