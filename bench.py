@@ -46,6 +46,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for the barrier / max-over-ranks plumbing (gloo: single-GPU tests)")
+    ap.add_argument("--crop", default=None, help="HxW: f3 partial-decode bench (random window + flip per image)")
+    ap.add_argument("--ablation", action="store_true",
+                    help="f2: time the paper's Fig. 10 decoder variants (u8) on the config, vs the production kernel")
     ap.add_argument("--share-device", action="store_true",
                     help="all ranks on cuda:0 (multi-rank plumbing tests on a 1-GPU box; not a scaling run)")
     return ap.parse_args()
@@ -192,10 +195,111 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_crop(args):
+    """f3: decode only a random HxW window (+ random flip) of every image — the patches the
+    window touches are the only ones read. Reports window Mpixel/s and the speed-up over full decode."""
+    import torch
+
+    from paper_2208_08711_b200 import BatchDecoder, encode_batch, normalize_constants
+    from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD
+    torch.cuda.set_device(0)
+    out_kind = args.out or ("f32" if args.config == "c3_cityscapes" else "u8")
+    dt = torch.float32 if out_kind == "f32" else torch.uint8
+    ch_, cw_ = (int(v) for v in args.crop.lower().split("x"))
+    imgs = rank_images(args.config, 0)
+    n = len(imgs)
+    src, offs = encode_batch(imgs)
+    srcs = [src] + [src.clone() for _ in range(ROTATE - 1)]
+    shapes_np = np.array([im.shape[1:] for im in imgs], np.int32)
+    shapes = torch.from_numpy(shapes_np).cuda()
+    rng = np.random.default_rng(7)
+    crops = np.array([[rng.integers(0, h - ch_ + 1), rng.integers(0, w - cw_ + 1), ch_, cw_, rng.integers(0, 2)]
+                      for h, w in shapes_np], np.int32)
+    crops_t = torch.from_numpy(crops).cuda()
+    scale, bias = normalize_constants(IMAGENET_MEAN, IMAGENET_STD) if out_kind == "f32" else ((1, 1, 1), (0, 0, 0))
+    out_c = torch.empty((n, 3, ch_, cw_), dtype=dt, device="cuda")
+    out_f = torch.empty(int(sum(3 * int(h) * int(w) for h, w in shapes_np)), dtype=dt, device="cuda")
+    oo = torch.from_numpy(np.concatenate([[0], np.cumsum(3 * shapes_np[:, 0].astype(np.int64) *
+                                                         shapes_np[:, 1])[:-1]]).astype(np.int64)).cuda()
+    dec = BatchDecoder(n)
+    stream = torch.cuda.Stream()
+    from paper_2208_08711_b200 import l3
+    a_c = [dec.args(x, offs, shapes, out_c, scale=scale, bias=bias, crops=crops_t) for x in srcs]
+    a_f = [dec.args(x, offs, shapes, out_f, out_offsets=oo, scale=scale, bias=bias) for x in srcs]
+
+    def timed(alist):
+        for i in range(args.warmup):
+            l3.l3_decode_batch(alist[i % ROTATE], stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            l3.l3_decode_batch(alist[i % ROTATE], stream)
+        e1.record(stream)
+        e1.synchronize()
+        assert bool((dec.status[:n] == 0).all())
+        return e0.elapsed_time(e1) / args.steps
+    ms_c, ms_f = timed(a_c), timed(a_f)
+    win_px = n * ch_ * cw_
+    line = {"metric": "decoded window Mpixel/s (partial decode, f3)", "value": round(win_px / (ms_c / 1e3) / 1e6, 3),
+            "unit": "Mpixel/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_c, 4), "higher_is_better": True, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": args.config + f": random {ch_}x{cw_} window + random flip per image, out "
+                       + out_kind, "batch": n},
+            "ms_full_decode": round(ms_f, 4), "speedup_vs_full_decode": round(ms_f / ms_c, 3),
+            "window_fraction_of_pixels": round(win_px / float((shapes_np[:, 0] * shapes_np[:, 1]).sum()), 4)}
+    print(json.dumps(line), flush=True)
+
+
+def run_ablation(args):
+    """f2 (Fig. 10): decode time of the paper's decoder variants on B200 (same format,
+    custom Paeth): patch-level only (thread per patch), +pixel-wise BD, +row-wise Paeth, both, and the
+    production kernel. All bit-exact (tests/test_gpu_parity.py::test_ablation_decoders_bit_exact)."""
+    import torch
+
+    from paper_2208_08711_b200 import BatchDecoder, encode_batch, l3
+    torch.cuda.set_device(0)
+    imgs = rank_images(args.config, 0)
+    n = len(imgs)
+    src, offs = encode_batch(imgs)
+    shapes_np = np.array([im.shape[1:] for im in imgs], np.int32)
+    shapes = torch.from_numpy(shapes_np).cuda()
+    sizes = 3 * shapes_np[:, 0].astype(np.int64) * shapes_np[:, 1]
+    oo = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)).cuda()
+    out = torch.empty(int(sizes.sum()), dtype=torch.uint8, device="cuda")
+    dec = BatchDecoder(n)
+    a = dec.args(src, offs, shapes, out, out_offsets=oo)
+    stream = torch.cuda.Stream()
+    steps = max(1, min(args.steps, 10))
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / steps
+    names = ["patch_level_only (thread/patch, seq BD, seq Paeth)", "+pixel_wise_BD", "+row_wise_custom_Paeth",
+             "+both (paper design, scalar)"]
+    res = {nm: round(timed(lambda m=m: l3.l3_decode_batch_ablation(a, m, stream)), 4) for m, nm in enumerate(names)}
+    res["production (l3_decode_batch)"] = round(timed(lambda: l3.l3_decode_batch(a, stream)), 4)
+    base = res[names[0]]
+    line = {"metric": "decode ms per batch (u8), paper Fig. 10 ablation on B200", "unit": "ms", "config": {
+        "workload": args.config, "batch": n}, "ms": res, "normalized_to_patch_level_only": {
+        k: round(v / base, 4) for k, v in res.items()}, "steps": steps}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.crop:
+        return run_crop(args)
+    if args.ablation:
+        return run_ablation(args)
 
     import torch
     import torch.distributed as dist

@@ -143,6 +143,17 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* args, const void* host_sr
 int32_t l3_decode_kernels_per_call(void);
 
 /*
+ * Ablation decoders (§5.5 Fig. 10), u8 output, valid files
+ * only (statuses cover the header; stream errors are not detected), for timing comparisons:
+ *   mode 0  one thread per patch, sequential base-delta + sequential custom Paeth
+ *   mode 1  one warp per patch, pixel-wise parallel base-delta, sequential Paeth
+ *   mode 2  one warp per patch, sequential base-delta, row-wise parallel Paeth
+ *   mode 3  one warp per patch, both parallel (the paper's design, plain scalar code)
+ * Same arguments as l3_decode_batch (out_kind must be L3_OUT_U8, crops NULL).
+ */
+l3_status_t l3_decode_batch_ablation(const l3_decode_args* args, int32_t mode, l3_stream_t stream);
+
+/*
  * Diagnostic: evaluates the decoder's device-side custom-Paeth predictor
  * (Fig. 3; ties TL, T, TR) on all 2^24 triples.
  * out: device, 2^24 bytes; out[TL<<16 | T<<8 | TR] = predicted byte.

@@ -1,0 +1,175 @@
+// l3_ablation.cu — the paper's decoder ablation (§5.5, Fig. 10 `fig:module`)
+// re-run on B200, on the same L3 format as the hot path.
+//
+// The paper's axes, all with patch-level parallelism (its "baseline" state):
+//   mode 0  one THREAD per patch: sequential base-delta decode + sequential Paeth
+//   mode 1  one WARP per patch: pixel-wise parallel BD, sequential Paeth (lane 0)
+//   mode 2  one WARP per patch: sequential BD (lane 0), row-wise parallel Paeth
+//   mode 3  one WARP per patch: both (the paper's full design, plain scalar code)
+// The paper's baseline uses the ORIGINAL (left/top/top-left) Paeth, a different file format;
+// here every mode decodes the custom-Paeth format, so mode 0 isolates the parallelisation
+// (DESIGN.md §7). The production kernel (l3_decode_batch) is the fifth bar.
+// Valid files only (the ablation reports time, not errors); reads stay inside each unit.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/l3.h"
+#include "l3_internal.cuh"
+
+namespace l3 {
+
+cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s);
+
+struct AblParams {
+  const uint8_t* src;
+  uint8_t* out;
+  const ImgDesc* desc;
+  const int32_t* status;
+  int n;
+};
+
+__device__ __forceinline__ uint32_t abl_u32le(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+// k bits at bit position pos of [data, data+len) MSB-first; 0 past the end.
+__device__ __forceinline__ uint32_t abl_bits(const uint8_t* data, uint64_t len, uint64_t pos, uint32_t k) {
+  uint32_t v = 0;
+  for (uint32_t i = 0; i < k; i++, pos++) {
+    const uint64_t b = pos >> 3;
+    const uint32_t bit = b < len ? (data[b] >> (7 - (pos & 7))) & 1u : 0u;
+    v = (v << 1) | bit;
+  }
+  return v;
+}
+
+struct AblUnit {
+  const uint8_t* data;
+  uint64_t len;
+  uint8_t* plane;
+  uint32_t W, x0, y0, w, h;
+};
+
+__device__ __forceinline__ bool abl_unit(const AblParams& p, int img, uint32_t u, AblUnit& U) {
+  const ImgDesc& d = p.desc[img];
+  const uint32_t nunits = 3u * d.P;
+  if (u >= nunits) return false;
+  const uint8_t* file = p.src + d.file_off;
+  const uint64_t off = abl_u32le(file + 13 + 4ull * u);
+  const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)abl_u32le(file + 17 + 4ull * u) : d.data_len;
+  if (nxt <= off || off >= d.data_len) return false;
+  const uint32_t ch = u / d.P, pp = u % d.P;
+  U.data = p.src + d.data_off + off;
+  U.len = nxt - off;
+  U.W = d.W;
+  U.x0 = (pp % d.gx) * d.N;
+  U.y0 = (pp / d.gx) * d.N;
+  U.w = min(d.N, d.W - U.x0);
+  U.h = min(d.N, d.H - U.y0);
+  U.plane = p.out + d.out_off + (uint64_t)ch * d.W * d.H;
+  return true;
+}
+
+// mode 0: one thread per patch, everything sequential
+__global__ void l3_ablation_thread_kernel(AblParams p) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int img = 0; img < p.n; img++) {
+    if (p.status[img] != L3_OK) continue;
+    for (uint32_t u = tid; u < 3u * p.desc[img].P; u += nth) {
+      AblUnit U;
+      if (!abl_unit(p, img, u, U)) continue;
+      uint64_t pos = 0;
+      for (uint32_t r = 0; r < U.h; r++) {
+        const uint32_t k = abl_bits(U.data, U.len, pos, 4), base = abl_bits(U.data, U.len, pos + 4, 8);
+        pos += 12;
+        uint8_t* row = U.plane + (uint64_t)(U.y0 + r) * U.W + U.x0;
+        for (uint32_t c = 0; c < U.w; c++, pos += k) {
+          const int res = (int)((base + abl_bits(U.data, U.len, pos, k)) & 0xFFu);
+          if (r == 0) {
+            row[c] = (uint8_t)res;
+          } else {
+            const uint8_t* up = row - U.W;
+            const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
+            row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res) & 0xFF);
+          }
+        }
+      }
+    }
+  }
+}
+
+// modes 1-3: one warp per patch; residuals of the current row pass through shared memory
+template <bool PAR_BD, bool PAR_PAETH>
+__global__ void l3_ablation_warp_kernel(AblParams p) {
+  __shared__ uint8_t res_s[8][256];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  uint8_t* res = res_s[wl];
+  for (int img = 0; img < p.n; img++) {
+    if (p.status[img] != L3_OK) continue;
+    for (uint32_t u = gw; u < 3u * p.desc[img].P; u += nw) {
+      AblUnit U;
+      if (!abl_unit(p, img, u, U)) continue;
+      uint64_t pos = 0;
+      for (uint32_t r = 0; r < U.h; r++) {
+        const uint32_t k = abl_bits(U.data, U.len, pos, 4), base = abl_bits(U.data, U.len, pos + 4, 8);
+        pos += 12;
+        // step 2 of PAPER.md:152: deltas + base
+        if (PAR_BD) {
+          for (uint32_t c = lane; c < U.w; c += 32)
+            res[c] = (uint8_t)((base + abl_bits(U.data, U.len, pos + (uint64_t)c * k, k)) & 0xFFu);
+        } else if (lane == 0) {
+          for (uint32_t c = 0; c < U.w; c++)
+            res[c] = (uint8_t)((base + abl_bits(U.data, U.len, pos + (uint64_t)c * k, k)) & 0xFFu);
+        }
+        __syncwarp();
+        pos += (uint64_t)k * U.w;
+        uint8_t* row = U.plane + (uint64_t)(U.y0 + r) * U.W + U.x0;
+        const uint8_t* up = row - U.W;
+        if (PAR_PAETH) {
+          for (uint32_t c = lane; c < U.w; c += 32) {
+            if (r == 0) {
+              row[c] = res[c];
+            } else {
+              const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
+              row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res[c]) & 0xFF);
+            }
+          }
+        } else if (lane == 0) {
+          for (uint32_t c = 0; c < U.w; c++) {
+            if (r == 0) {
+              row[c] = res[c];
+            } else {
+              const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
+              row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res[c]) & 0xFF);
+            }
+          }
+        }
+        __syncwarp();
+        __threadfence_block();   // row r visible to all lanes before row r+1 reads it
+      }
+    }
+  }
+}
+
+cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s) {
+  cudaError_t e = launch_parse(a, s);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  AblParams p;
+  p.src = a->src;
+  p.out = reinterpret_cast<uint8_t*>(a->out);
+  const WsView ws = WsView::at(a->workspace, a->n);
+  p.desc = ws.desc;
+  p.status = a->status;
+  p.n = a->n;
+  if (mode == 0) l3_ablation_thread_kernel<<<sms * 8, 128, 0, s>>>(p);
+  else if (mode == 1) l3_ablation_warp_kernel<true, false><<<sms * 8, 256, 0, s>>>(p);
+  else if (mode == 2) l3_ablation_warp_kernel<false, true><<<sms * 8, 256, 0, s>>>(p);
+  else l3_ablation_warp_kernel<true, true><<<sms * 8, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace l3

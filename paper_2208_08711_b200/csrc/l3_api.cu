@@ -9,6 +9,7 @@ namespace l3 {
 cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s);
 cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s);
 cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s);
+cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s);
 uint64_t encode_workspace_size(const int32_t* shapes, const int32_t* n_host, int32_t n);
 l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s);
 }  // namespace l3
@@ -58,6 +59,13 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* a, const void* host_src, 
       cudaSuccess)
     return L3_E_CUDA;
   return L3_OK;
+}
+
+l3_status_t l3_decode_batch_ablation(const l3_decode_args* a, int32_t mode, l3_stream_t stream) {
+  l3_status_t st = check_decode_args(a);
+  if (st != L3_OK || a->n == 0) return st;
+  if (mode < 0 || mode > 3 || a->out_kind != L3_OUT_U8 || a->crops) return L3_E_INVALID_ARGUMENT;
+  return l3::launch_ablation(a, mode, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
 l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream) {

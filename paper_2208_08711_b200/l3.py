@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
             L.l3_decode_workspace_size.restype = ctypes.c_uint64
             L.l3_decode_kernels_per_call.argtypes = []
             L.l3_decode_kernels_per_call.restype = ctypes.c_int32
+            L.l3_decode_batch_ablation.argtypes = [P(l3_decode_args), ctypes.c_int32, ctypes.c_void_p]
+            L.l3_decode_batch_ablation.restype = ctypes.c_int
             L.l3_selftest_paeth.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
             L.l3_selftest_paeth.restype = ctypes.c_int
             L.l3_status_string.argtypes = [ctypes.c_int32]
@@ -115,7 +117,8 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ("l3_decode_workspace_size", "l3_decode_batch", "l3_parse_batch",
             "l3_load_decode_batch", "l3_decode_kernels_per_call", "l3_status_string", "l3_choose_patch_size",
-            "l3_encode_max_bytes", "l3_encode_workspace_size", "l3_encode_batch", "l3_selftest_paeth")
+            "l3_encode_max_bytes", "l3_encode_workspace_size", "l3_encode_batch", "l3_selftest_paeth",
+            "l3_decode_batch_ablation")
 
 
 def _dev_ptr(t: torch.Tensor | None, name: str, dtype=None) -> int:
@@ -190,6 +193,10 @@ def l3_load_decode_batch(args: l3_decode_args, host_src: torch.Tensor, host_stat
     _check("l3_load_decode_batch",
            lib().l3_load_decode_batch(ctypes.byref(args), host_src.data_ptr(), host_src.numel(),
                                       host_status.data_ptr(), _stream(stream)))
+
+
+def l3_decode_batch_ablation(args: l3_decode_args, mode: int, stream=None) -> None:
+    _check("l3_decode_batch_ablation", lib().l3_decode_batch_ablation(ctypes.byref(args), int(mode), _stream(stream)))
 
 
 def l3_selftest_paeth(out: torch.Tensor, stream=None) -> None:

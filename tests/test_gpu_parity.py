@@ -370,3 +370,25 @@ def test_crop_skips_patches_outside_the_window():
     assert st.tolist() == [0] and np.array_equal(got[0], im[:, :64, :64])
     got, st = _crop_decode([bytes(f)], [(256, 256)], [(192, 192, 64, 64, 0)])
     assert st.tolist() == [4]
+
+
+# ------------------------------------------------------------------ f2: ablation decoders
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_ablation_decoders_bit_exact(mode):
+    from paper_2208_08711_b200 import l3
+    imgs = [l3synth.uniform_image(h, w, s) for s, (h, w) in enumerate([(70, 133), (300, 260), (64, 64), (1, 5)])]
+    Ns = [32, 128, 64, 200]
+    files = [l3ref.encode(im, N=N) for im, N in zip(imgs, Ns)]
+    src, offs = pack_files(files)
+    sizes = [im.size for im in imgs]
+    oo = torch.tensor(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64), device="cuda")
+    out = torch.full((sum(sizes),), 0xA5, dtype=torch.uint8, device="cuda")
+    dec = BatchDecoder(len(files))
+    sh = torch.tensor([im.shape[1:] for im in imgs], dtype=torch.int32, device="cuda")
+    a = dec.args(src, offs, sh, out, out_offsets=oo)
+    l3.l3_decode_batch_ablation(a, mode)
+    torch.cuda.synchronize()
+    flat = out.cpu().numpy()
+    for o, s, im in zip(oo.cpu().numpy(), sizes, imgs):
+        assert np.array_equal(flat[o:o + s].reshape(im.shape), im)
