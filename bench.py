@@ -347,6 +347,8 @@ def main():
     dec = BatchDecoder(n, device=dev)
     stream = torch.cuda.Stream(device=dev)
     wide = wide_hint(shapes_np, out_dtype)
+    if os.environ.get("L3_FORCE_WIDE") in ("0", "1"):   # dev A/B of the kernel variant
+        wide = os.environ["L3_FORCE_WIDE"] == "1"
     args_list = [dec.args(s, offs, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide)
                  for s in srcs]
 

@@ -17,6 +17,7 @@
 // DESIGN.md §5 explains the mapping and its roofline.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "l3_internal.cuh"
 
@@ -511,7 +512,7 @@ cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
 
 // ============================================================== host launch
 static int g_sm_count = 0;
-static int g_occ[5] = {0, 0, 0, 0, 0};   // f32, u8 narrow, u8 wide, f32 crop, u8 crop
+static int g_occ[6] = {0, 0, 0, 0, 0, 0};   // f32, u8 narrow, u8 wide, f32 crop, u8 crop, f32 wide
 
 template <bool F32, bool WIDE, bool CROP>
 static int fused_occupancy() {
@@ -535,6 +536,7 @@ cudaError_t ensure_device_info() {
     g_occ[2] = fused_occupancy<false, true, false>();
     g_occ[3] = fused_occupancy<true, false, true>();
     g_occ[4] = fused_occupancy<false, false, true>();
+    g_occ[5] = fused_occupancy<true, true, false>();
   }
   return cudaSuccess;
 }
@@ -574,9 +576,14 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
   const bool crop = a->crops != nullptr;
-  const bool wide = !f32 && !crop && (a->flags & L3_DECODE_HINT_WIDE);
-  const int variant = crop ? (f32 ? 3 : 4) : (f32 ? 0 : (wide ? 2 : 1));
-  const int grid = g_sm_count * g_occ[variant];
+  const bool wide = !crop && (a->flags & L3_DECODE_HINT_WIDE);
+  const int variant = crop ? (f32 ? 3 : 4) : (f32 ? (wide ? 5 : 0) : (wide ? 2 : 1));
+  int ctas = g_occ[variant];
+  if (const char* e = getenv("L3_DEV_CTAS_PER_SM")) {   // dev-only A/B of the persistent grid
+    const int v = atoi(e);
+    if (v > 0 && v < ctas) ctas = v;
+  }
+  const int grid = g_sm_count * ctas;
   dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
   dp.pp.wide = wide ? 1u : 0u;
   const size_t smem = fast_smem_bytes();
@@ -586,7 +593,8 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
     case 1: l3_decode_kernel<false, false, false><<<grid, B, smem, s>>>(dp); break;
     case 2: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
     case 3: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
-    default: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
+    case 4: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
+    default: l3_decode_kernel<true, true, false><<<grid, B, smem, s>>>(dp); break;
   }
   return cudaGetLastError();
 }
