@@ -392,3 +392,71 @@ def test_ablation_decoders_bit_exact(mode):
     flat = out.cpu().numpy()
     for o, s, im in zip(oo.cpu().numpy(), sizes, imgs):
         assert np.array_equal(flat[o:o + s].reshape(im.shape), im)
+
+
+# ------------------------------------------------------------------ edge cases: sizes and counts
+
+def test_empty_batch_is_a_noop():
+    from paper_2208_08711_b200 import l3
+    dec = BatchDecoder(4)
+    src = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    offs = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sh = torch.zeros((0, 2), dtype=torch.int32, device="cuda")
+    out = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    l3.l3_decode_batch(dec.args(src, offs, sh, out))
+    torch.cuda.synchronize()
+
+
+def test_zero_length_and_tiny_files():
+    im = l3synth.natural(9, 11, 0, 1.0)
+    f = l3ref.encode(im)
+    files = [b"", b"L", f, b"L3IF", f[:13], f]
+    _, st, bad, _, _, _ = gpu_decode(files, [(9, 11)] * len(files))
+    ref = [l3ref.decode(x, exp_shape=(9, 11))[:2] for x in files]
+    assert [(int(a), int(b)) for a, b in zip(st, bad)] == [(int(a), int(b)) for a, b in ref]
+
+
+@pytest.mark.parametrize("n", [1500])
+def test_many_images_multi_chunk_parse(n):
+    """n > 1024 images: the work decomposition scans in chunks (carry across chunks)."""
+    rng = np.random.default_rng(9)
+    imgs, files = [], []
+    for i in range(n):
+        H, W = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        im = l3synth.uniform_image(H, W, i)
+        imgs.append(im)
+        files.append(l3ref.encode(im, N=int(rng.choice([0, 4, 16, 33, 64, 129]))))
+    for wide in (False, True):
+        got, st, _, _, _, _ = gpu_decode(files, [im.shape[1:] for im in imgs], wide=wide)
+        assert (st == 0).all()
+        for g, r in zip(got, imgs):
+            assert np.array_equal(g, r)
+
+
+def test_output_offset_beyond_2_31():
+    """Image blocks placed past element 2^31 of a 2.2 GB output: 64-bit output addressing."""
+    imgs = [l3synth.natural(130, 260, 1, 2.0), l3synth.natural(64, 200, 2, 2.0)]
+    files = [l3ref.encode(im) for im in imgs]
+    src, offs = pack_files(files)
+    base = (1 << 31) + 12345
+    sizes = [im.size for im in imgs]
+    out = torch.zeros(base + sum(sizes) + 16, dtype=torch.uint8, device="cuda")
+    oo = torch.tensor([base, base + sizes[0]], dtype=torch.int64, device="cuda")
+    sh = torch.tensor([im.shape[1:] for im in imgs], dtype=torch.int32, device="cuda")
+    dec = BatchDecoder(2)
+    st, _ = dec.decode(src, offs, sh, out, out_offsets=oo)
+    torch.cuda.synchronize()
+    assert st.tolist() == [0, 0]
+    for o, s, im in zip([base, base + sizes[0]], sizes, imgs):
+        assert np.array_equal(out[o:o + s].cpu().numpy().reshape(im.shape), im)
+    assert int(out[:base].count_nonzero()) == 0
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_large_single_image():
+    """One 8192x6144 image (150 MB raw, 3 x 3072 patches of 128x128)."""
+    im = l3synth.natural(6144, 8192, 5, 1.0)
+    f = l3ref.encode(im)
+    got, st, _, _, _, _ = gpu_decode([f], [im.shape[1:]])
+    assert st.tolist() == [0] and np.array_equal(got[0], im)
