@@ -44,9 +44,29 @@ int l3ref_predict(int tl, int t, int tr) {
   return cand[best];
 }
 
+/*
+ * The ORIGINAL Paeth predictor ("the original Paeth filter encodes each
+ * pixel based on three neighboring pixels (left, top, top-left)"), as defined for PNG:
+ * p = a + b - c; the neighbour closest to p, ties in the order a (left), b (top),
+ * c (top-left). Used only by the ablation format variant "L3IP" (reading
+ * C16 in DESIGN.md: missing left / top-left neighbours at column 0 are 0, as in PNG).
+ */
+int l3ref_predict_png(int a, int b, int c) {
+  int p = a + b - c;
+  int pa = iabs_(p - a), pb = iabs_(p - b), pc = iabs_(p - c);
+  if (pa <= pb && pa <= pc) return a;
+  if (pb <= pc) return b;
+  return c;
+}
+
 /* Element-wise l3ref_predict over arrays (lets tests sweep all 2^24 triples). */
 void l3ref_predict_many(const uint8_t* tl, const uint8_t* t, const uint8_t* tr, uint64_t n, uint8_t* out) {
   for (uint64_t i = 0; i < n; i++) out[i] = (uint8_t)l3ref_predict(tl[i], t[i], tr[i]);
+}
+
+/* Element-wise l3ref_predict_png (a = left, b = top, c = top-left). */
+void l3ref_predict_png_many(const uint8_t* a, const uint8_t* b, const uint8_t* c, uint64_t n, uint8_t* out) {
+  for (uint64_t i = 0; i < n; i++) out[i] = (uint8_t)l3ref_predict_png(a[i], b[i], c[i]);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -167,8 +187,22 @@ static uint32_t get_u32le_(const uint8_t* p) {
 /* Encoder: §4.2 two stages per patch, §4.3 container     */
 /* ------------------------------------------------------------------------ */
 
+static uint64_t encode_image_(const uint8_t* planar, uint32_t W, uint32_t H, int N, int base_rule, int k_extra,
+                              int predictor, uint8_t* out, uint64_t cap);
+
 uint64_t l3ref_encode_image(const uint8_t* planar, uint32_t W, uint32_t H, int N,
                             int base_rule, int k_extra, uint8_t* out, uint64_t cap) {
+  return encode_image_(planar, W, H, N, base_rule, k_extra, 0, out, cap);
+}
+
+/* Ablation variant (f2): predictor 1 = original Paeth, file magic "L3IP". */
+uint64_t l3ref_encode_image_variant(const uint8_t* planar, uint32_t W, uint32_t H, int N, int predictor,
+                                    uint8_t* out, uint64_t cap) {
+  return encode_image_(planar, W, H, N, L3REF_BASE_SIGNED, 0, predictor, out, cap);
+}
+
+static uint64_t encode_image_(const uint8_t* planar, uint32_t W, uint32_t H, int N, int base_rule, int k_extra,
+                              int predictor, uint8_t* out, uint64_t cap) {
   if (W == 0 || H == 0 || N < 0 || N > 255) return 0;
   if (N == 0) N = l3ref_choose_patch_size(W, H);
   uint64_t gx = ceil_div_(W, (uint64_t)N), gy = ceil_div_(H, (uint64_t)N);
@@ -177,7 +211,7 @@ uint64_t l3ref_encode_image(const uint8_t* planar, uint32_t W, uint32_t H, int N
   if (cap < hdr) return 0;
   memset(out, 0, (size_t)cap);
   /* Fig. 5: magic (4 B), width (4 B), height (4 B), patch size (1 B), 3 offset arrays */
-  memcpy(out, "L3IF", 4);
+  memcpy(out, predictor ? "L3IP" : "L3IF", 4);
   put_u32le_(out + 4, W);
   put_u32le_(out + 8, H);
   out[12] = (uint8_t)N;
@@ -211,10 +245,19 @@ uint64_t l3ref_encode_image(const uint8_t* planar, uint32_t W, uint32_t H, int N
       for (int c = 0; c < w; c++) resid[c] = patch[c];
       for (int r = 1; r < h; r++) {
         for (int c = 0; c < w; c++) {
-          int t = patch[(r - 1) * w + c];
-          int tl = c > 0 ? patch[(r - 1) * w + c - 1] : t;
-          int tr = c < w - 1 ? patch[(r - 1) * w + c + 1] : t;
-          resid[r * w + c] = (uint8_t)((patch[r * w + c] - l3ref_predict(tl, t, tr)) & 0xFF);
+          int pred;
+          if (predictor == 0) {
+            int t = patch[(r - 1) * w + c];
+            int tl = c > 0 ? patch[(r - 1) * w + c - 1] : t;
+            int tr = c < w - 1 ? patch[(r - 1) * w + c + 1] : t;
+            pred = l3ref_predict(tl, t, tr);
+          } else {   /* original Paeth: left, top, top-left of the SAME patch (0 when absent) */
+            int a = c > 0 ? patch[r * w + c - 1] : 0;
+            int b = patch[(r - 1) * w + c];
+            int cc = c > 0 ? patch[(r - 1) * w + c - 1] : 0;
+            pred = l3ref_predict_png(a, b, cc);
+          }
+          resid[r * w + c] = (uint8_t)((patch[r * w + c] - pred) & 0xFF);
         }
       }
 
@@ -248,14 +291,23 @@ typedef struct {
   uint64_t gx, gy, P;
   uint64_t hdr, data_len;
   const uint8_t* data;
+  int predictor;   /* 0 custom (L3IF), 1 original Paeth (L3IP, ablation variant) */
 } l3hdr;
 
 /* Reading a1 / C9: header parse and validation order:
  *   magic -> UNRECOGNIZED_FORMAT; short header, W/H/N zero, shape mismatch,
  *   offsets table outside the file, offsets not starting at 0 / not strictly
  *   increasing over R||G||B / not inside the data section -> CORRUPT_HEADER. */
+static int parse_header_v_(const uint8_t* f, uint64_t len, uint32_t exp_W, uint32_t exp_H, l3hdr* h,
+                           int allow_variant);
 static int parse_header_(const uint8_t* f, uint64_t len, uint32_t exp_W, uint32_t exp_H, l3hdr* h) {
-  if (len < 4 || memcmp(f, "L3IF", 4) != 0) return L3REF_E_UNRECOGNIZED_FORMAT;
+  return parse_header_v_(f, len, exp_W, exp_H, h, 0);
+}
+static int parse_header_v_(const uint8_t* f, uint64_t len, uint32_t exp_W, uint32_t exp_H, l3hdr* h,
+                           int allow_variant) {
+  h->predictor = 0;
+  if (len >= 4 && allow_variant && memcmp(f, "L3IP", 4) == 0) h->predictor = 1;
+  else if (len < 4 || memcmp(f, "L3IF", 4) != 0) return L3REF_E_UNRECOGNIZED_FORMAT;
   if (len < 13) return L3REF_E_CORRUPT_HEADER;
   h->W = get_u32le_(f + 4);
   h->H = get_u32le_(f + 8);
@@ -318,10 +370,16 @@ static int decode_unit_(const l3hdr* h, const uint8_t* file, uint64_t u, uint8_t
        * residual ... to the pixel value" */
       const uint8_t* up = row - h->W;
       for (int c = 0; c < w; c++) {
-        int t = up[c];
-        int tl = c > 0 ? up[c - 1] : t;
-        int tr = c < w - 1 ? up[c + 1] : t;
-        row[c] = (uint8_t)((l3ref_predict(tl, t, tr) + res[c]) & 0xFF);
+        if (h->predictor == 0) {
+          int t = up[c];
+          int tl = c > 0 ? up[c - 1] : t;
+          int tr = c < w - 1 ? up[c + 1] : t;
+          row[c] = (uint8_t)((l3ref_predict(tl, t, tr) + res[c]) & 0xFF);
+        } else {   /* original Paeth: depends on the pixel just decoded to the left */
+          int a = c > 0 ? row[c - 1] : 0;
+          int cc = c > 0 ? up[c - 1] : 0;
+          row[c] = (uint8_t)((l3ref_predict_png(a, up[c], cc) + res[c]) & 0xFF);
+        }
       }
     }
   }
@@ -329,13 +387,29 @@ static int decode_unit_(const l3hdr* h, const uint8_t* file, uint64_t u, uint8_t
   return L3REF_OK;
 }
 
+static int decode_image_(const uint8_t* file, uint64_t len, uint32_t exp_W, uint32_t exp_H, uint8_t* out,
+                         uint64_t out_cap, int64_t* bad_unit, uint32_t* W, uint32_t* H, int* N, uint64_t* P,
+                         int allow_variant);
+
 int l3ref_decode_image(const uint8_t* file, uint64_t len, uint32_t exp_W, uint32_t exp_H,
                        uint8_t* out, uint64_t out_cap, int64_t* bad_unit,
                        uint32_t* W, uint32_t* H, int* N, uint64_t* P) {
+  return decode_image_(file, len, exp_W, exp_H, out, out_cap, bad_unit, W, H, N, P, 0);
+}
+
+/* Accepts both "L3IF" and the ablation variant "L3IP" (original Paeth). */
+int l3ref_decode_image_variant(const uint8_t* file, uint64_t len, uint8_t* out, uint64_t out_cap,
+                               uint32_t* W, uint32_t* H) {
+  return decode_image_(file, len, 0, 0, out, out_cap, NULL, W, H, NULL, NULL, 1);
+}
+
+static int decode_image_(const uint8_t* file, uint64_t len, uint32_t exp_W, uint32_t exp_H, uint8_t* out,
+                         uint64_t out_cap, int64_t* bad_unit, uint32_t* W, uint32_t* H, int* N, uint64_t* P,
+                         int allow_variant) {
   l3hdr h;
   memset(&h, 0, sizeof h);
   if (bad_unit) *bad_unit = -1;
-  int st = parse_header_(file, len, exp_W, exp_H, &h);
+  int st = parse_header_v_(file, len, exp_W, exp_H, &h, allow_variant);
   if (W) *W = h.W;
   if (H) *H = h.H;
   if (N) *N = h.N;

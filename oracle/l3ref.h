@@ -36,6 +36,8 @@ enum { L3REF_BASE_SIGNED = 0, L3REF_BASE_UNSIGNED = 1 };
 
 /* PAPER.md:135-137 (§4.2, Fig. 3): custom Paeth predictor over the previous row. */
 int l3ref_predict(int tl, int t, int tr);
+int l3ref_predict_png(int a, int b, int c);
+void l3ref_predict_png_many(const uint8_t* a, const uint8_t* b, const uint8_t* c, uint64_t n, uint8_t* out);
 void l3ref_predict_many(const uint8_t* tl, const uint8_t* t, const uint8_t* tr, uint64_t n, uint8_t* out);
 
 /* PAPER.md:166 (§4.3): patch-size policy, reading C10. */
@@ -55,6 +57,12 @@ uint64_t l3ref_max_file_bytes(uint32_t W, uint32_t H, int N);
  */
 uint64_t l3ref_encode_image(const uint8_t* planar, uint32_t W, uint32_t H, int N,
                             int base_rule, int k_extra, uint8_t* out, uint64_t cap);
+
+/* Ablation variant: predictor 1 = original (left/top/top-left) Paeth, magic "L3IP". */
+uint64_t l3ref_encode_image_variant(const uint8_t* planar, uint32_t W, uint32_t H, int N, int predictor,
+                                    uint8_t* out, uint64_t cap);
+int l3ref_decode_image_variant(const uint8_t* file, uint64_t len, uint8_t* out, uint64_t out_cap,
+                               uint32_t* W, uint32_t* H);
 
 /*
  * Sequential decode of one L3 file.

@@ -48,6 +48,16 @@ def lib():
             L.l3ref_predict.restype = ctypes.c_int
             L.l3ref_predict_many.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint64, ctypes.c_void_p]
             L.l3ref_predict_many.restype = None
+            L.l3ref_predict_png_many.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint64, ctypes.c_void_p]
+            L.l3ref_predict_png_many.restype = None
+            L.l3ref_predict_png.argtypes = [ctypes.c_int] * 3
+            L.l3ref_predict_png.restype = ctypes.c_int
+            L.l3ref_encode_image_variant.argtypes = [u8p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
+                                                     ctypes.c_int, u8p, ctypes.c_uint64]
+            L.l3ref_encode_image_variant.restype = ctypes.c_uint64
+            L.l3ref_decode_image_variant.argtypes = [u8p, ctypes.c_uint64, u8p, ctypes.c_uint64,
+                                                     ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]
+            L.l3ref_decode_image_variant.restype = ctypes.c_int
             L.l3ref_choose_patch_size.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
             L.l3ref_choose_patch_size.restype = ctypes.c_int
             L.l3ref_bd_encode_row.argtypes = [u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -89,6 +99,13 @@ def predict_many(tl: np.ndarray, t: np.ndarray, tr: np.ndarray) -> np.ndarray:
     return out
 
 
+def predict_png_many(a: np.ndarray, b: np.ndarray, c: np.ndarray) -> np.ndarray:
+    a, b, c = (np.ascontiguousarray(x, np.uint8) for x in (a, b, c))
+    out = np.zeros(len(a), np.uint8)
+    lib().l3ref_predict_png_many(a.ctypes.data, b.ctypes.data, c.ctypes.data, len(a), out.ctypes.data)
+    return out
+
+
 def choose_patch_size(W: int, H: int) -> int:
     return lib().l3ref_choose_patch_size(W, H)
 
@@ -117,6 +134,32 @@ def encode(planar: np.ndarray, N: int = 0, base_rule: int = BASE_SIGNED, k_extra
     if n == 0:
         raise ValueError("l3ref_encode_image failed")
     return out[:n].tobytes()
+
+
+def predict_png(a: int, b: int, c: int) -> int:
+    return lib().l3ref_predict_png(a, b, c)
+
+
+def encode_variant(planar: np.ndarray, N: int = 0, predictor: int = 1) -> bytes:
+    """Ablation format variant (f2): predictor 1 = original Paeth (magic "L3IP")."""
+    planar = np.ascontiguousarray(planar, dtype=np.uint8)
+    _, H, W = planar.shape
+    cap = max_file_bytes(W, H, N)
+    out = np.zeros(cap, np.uint8)
+    n = lib().l3ref_encode_image_variant(_u8(planar), W, H, N, predictor, _u8(out), cap)
+    if n == 0:
+        raise ValueError("l3ref_encode_image_variant failed")
+    return out[:n].tobytes()
+
+
+def decode_variant(data: bytes, shape):
+    """Decode an L3IF or L3IP file of known shape (H, W). Returns (status, planar)."""
+    H, W = shape
+    buf = np.frombuffer(data, np.uint8)
+    out = np.zeros((3, H, W), np.uint8)
+    w, h = ctypes.c_uint32(), ctypes.c_uint32()
+    st = lib().l3ref_decode_image_variant(_u8(buf), len(data), _u8(out), out.size, ctypes.byref(w), ctypes.byref(h))
+    return st, out
 
 
 def decode(data: bytes, exp_shape=None):

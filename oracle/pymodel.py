@@ -19,6 +19,25 @@ def predict(tl: int, t: int, tr: int) -> int:
     return ranked[0][2]
 
 
+def predict_png(a: int, b: int, c: int) -> int:
+    """PNG Paeth (original L3 ablation baseline): closest to a+b-c, ties a, b, c."""
+    p = a + b - c
+    return sorted([(abs(p - a), 0, a), (abs(p - b), 1, b), (abs(p - c), 2, c)])[0][2]
+
+
+def filter_patch_png(patch):
+    """Original-Paeth residuals of a patch: row 0 raw; left / top-left are 0 at column 0 (reading C16)."""
+    out = [list(patch[0])]
+    for r in range(1, len(patch)):
+        row = []
+        for c in range(len(patch[r])):
+            a = patch[r][c - 1] if c else 0
+            cc = patch[r - 1][c - 1] if c else 0
+            row.append((patch[r][c] - predict_png(a, patch[r - 1][c], cc)) % 256)
+        out.append(row)
+    return out
+
+
 def _neighbours(prev, c):
     w = len(prev)
     t = prev[c]
@@ -45,8 +64,9 @@ def bd_row(res, first_row: bool, signed_rule: bool = True):
     return k, base, [(v - base) % 256 for v in res]
 
 
-def encode(planar, N: int, signed_rule: bool = True) -> bytes:
-    """planar: [3][H][W] nested lists. Returns L3 file bytes (C8, C9)."""
+def encode(planar, N: int, signed_rule: bool = True, predictor: int = 0) -> bytes:
+    """planar: [3][H][W] nested lists. Returns L3 file bytes (C8, C9).
+    predictor 1 = original Paeth ablation variant, magic "L3IP" (reading C16)."""
     H, W = len(planar[0]), len(planar[0][0])
     gx, gy = -(-W // N), -(-H // N)
     P = gx * gy
@@ -56,7 +76,7 @@ def encode(planar, N: int, signed_rule: bool = True) -> bytes:
             x0, y0 = (p % gx) * N, (p // gx) * N
             patch = [row[x0:x0 + N] for row in planar[ch][y0:y0 + N]]
             bits = ""
-            for r, rres in enumerate(filter_patch(patch)):
+            for r, rres in enumerate(filter_patch_png(patch) if predictor else filter_patch(patch)):
                 k, base, deltas = bd_row(rres, r == 0, signed_rule)
                 bits += format(k, "04b") + format(base, "08b") + "".join(format(d, f"0{k}b") for d in deltas)
             bits += "0" * (-len(bits) % 8)                # byte-align each patch
@@ -67,12 +87,14 @@ def encode(planar, N: int, signed_rule: bool = True) -> bytes:
         chunk = bytes(int(bits[i:i + 8], 2) for i in range(0, len(bits), 8))
         data += chunk
         pos += len(chunk)
-    return b"L3IF" + struct.pack("<IIB", W, H, N) + struct.pack(f"<{3 * P}I", *offsets) + data
+    magic = b"L3IP" if predictor else b"L3IF"
+    return magic + struct.pack("<IIB", W, H, N) + struct.pack(f"<{3 * P}I", *offsets) + data
 
 
 def decode(blob: bytes):
     """Returns [3][H][W] nested lists (valid files only)."""
-    assert blob[:4] == b"L3IF"
+    assert blob[:4] in (b"L3IF", b"L3IP")
+    png = blob[:4] == b"L3IP"
     W, H, N = struct.unpack("<IIB", blob[4:13])
     gx, gy = -(-W // N), -(-H // N)
     P = gx * gy
@@ -95,7 +117,16 @@ def decode(blob: bytes):
             for _ in range(w):
                 res.append((base + int(bits[pos:pos + k], 2)) % 256)
                 pos += k
-            row = res if prev is None else [(predict(*_neighbours(prev, c)) + res[c]) % 256 for c in range(w)]
+            if prev is None:
+                row = res
+            elif png:
+                row = []
+                for c in range(w):
+                    a = row[c - 1] if c else 0
+                    cc = prev[c - 1] if c else 0
+                    row.append((predict_png(a, prev[c], cc) + res[c]) % 256)
+            else:
+                row = [(predict(*_neighbours(prev, c)) + res[c]) % 256 for c in range(w)]
             out[ch][y0 + r][x0:x0 + w] = row
             prev = row
     return out
