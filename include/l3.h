@@ -145,10 +145,15 @@ int32_t l3_decode_kernels_per_call(void);
 /*
  * Ablation decoders (§5.5 Fig. 10), u8 output, valid files
  * only (statuses cover the header; stream errors are not detected), for timing comparisons:
- *   mode 0  one thread per patch, sequential base-delta + sequential custom Paeth
+ *   mode 0  one thread per patch, sequential base-delta + sequential Paeth
  *   mode 1  one warp per patch, pixel-wise parallel base-delta, sequential Paeth
  *   mode 2  one warp per patch, sequential base-delta, row-wise parallel Paeth
  *   mode 3  one warp per patch, both parallel (the paper's design, plain scalar code)
+ *   mode 4  one warp per patch, sequential base-delta + sequential Paeth (lane 0)
+ * Modes 0, 1 and 4 also read the original-Paeth variant "L3IP" (per image, by magic; reading
+ * C16), so the paper's Baseline / +Pixel-wise BD bars are modes 0 / 1 on L3IP files. Modes 2
+ * and 3 cannot (the left dependency forbids a row-parallel Paeth) and set L3IP images to
+ * L3_E_UNRECOGNIZED_FORMAT. Other modes: L3_E_INVALID_ARGUMENT.
  * Same arguments as l3_decode_batch (out_kind must be L3_OUT_U8, crops NULL).
  */
 l3_status_t l3_decode_batch_ablation(const l3_decode_args* args, int32_t mode, l3_stream_t stream);
@@ -183,6 +188,11 @@ uint64_t l3_encode_max_bytes(uint32_t W, uint32_t H, int32_t N);
  *   n_host       host, n patch sizes (0 = policy) or NULL (policy for all).
  *   dst          device, dst_capacity >= sum of l3_encode_max_bytes.
  *   dst_offsets  device, n+1 uint64, written: file i = dst[dst_offsets[i] .. dst_offsets[i+1]).
+ *   predictor    0: the custom Paeth of PAPER.md:137 (magic "L3IF", the hot path's format).
+ *                1: the ORIGINAL left/top/top-left Paeth, magic "L3IP": the
+ *                   format of the paper's ablation baseline (Fig. 10), readable only by
+ *                   l3_decode_batch_ablation modes 0 and 1 (reading C16).
+ *                Other values: L3_E_INVALID_ARGUMENT.
  */
 typedef struct {
   const uint8_t* images;
@@ -195,6 +205,7 @@ typedef struct {
   uint64_t* dst_offsets;
   void* workspace;
   uint64_t workspace_bytes;
+  int32_t predictor;
 } l3_encode_args;
 
 /* Device workspace bytes for l3_encode_batch (depends on the host shapes). */

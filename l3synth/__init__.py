@@ -96,6 +96,9 @@ CONFIGS = {
     "c2_imagenet": dict(n=256, shape=None, kind="natural", gain="imagenet", seed0=1000),
     "c3_cityscapes": dict(n=32, shape=(1024, 2048), kind="natural", gain="cityscapes", seed0=2000),
     "c4_uhd": dict(n=16, shape=(2160, 3840), kind="natural", gain="uhd", seed0=3000),
+    # ablation-only workloads (the Fig. 10 study rescales Cityscapes to HD / FHD / UHD)
+    "ab_hd": dict(n=32, shape=(720, 1280), kind="natural", gain="cityscapes", seed0=4000),
+    "ab_fhd": dict(n=32, shape=(1080, 1920), kind="natural", gain="cityscapes", seed0=5000),
 }
 
 

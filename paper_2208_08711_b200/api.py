@@ -93,8 +93,9 @@ def pack_files(files: Sequence[bytes], device="cuda"):
 
 
 def encode_batch(images: Sequence[np.ndarray] | Sequence[torch.Tensor], patch_sizes=None, device="cuda",
-                 stream=None):
-    """GPU-encode planar uint8 [3, H, W] images. Returns (src, src_offsets) on device."""
+                 stream=None, predictor: int = 0):
+    """GPU-encode planar uint8 [3, H, W] images. Returns (src, src_offsets) on device.
+    predictor=1 writes the original-Paeth ablation variant "L3IP" (reading C16)."""
     n = len(images)
     shapes = np.array([tuple(im.shape[1:]) for im in images], np.int32).reshape(n, 2)
     sizes = np.array([3 * int(h) * int(w) for h, w in shapes], np.int64)
@@ -111,7 +112,7 @@ def encode_batch(images: Sequence[np.ndarray] | Sequence[torch.Tensor], patch_si
     dst = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
     dst_offsets = torch.empty(n + 1, dtype=torch.int64, device=device)
     ws = torch.empty(max(l3.l3_encode_workspace_size(shapes, nh), 256), dtype=torch.uint8, device=device)
-    l3.l3_encode_batch(flat, img_off, shapes, nh, dst, dst_offsets, ws, stream)
+    l3.l3_encode_batch(flat, img_off, shapes, nh, dst, dst_offsets, ws, stream, predictor=predictor)
     torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
     total = int(dst_offsets[-1].item())
     src = torch.empty(max(total, 1), dtype=torch.uint8, device=device)

@@ -6,9 +6,14 @@
 //   mode 1  one WARP per patch: pixel-wise parallel BD, sequential Paeth (lane 0)
 //   mode 2  one WARP per patch: sequential BD (lane 0), row-wise parallel Paeth
 //   mode 3  one WARP per patch: both (the paper's full design, plain scalar code)
-// The paper's baseline uses the ORIGINAL (left/top/top-left) Paeth, a different file format;
-// here every mode decodes the custom-Paeth format, so mode 0 isolates the parallelisation
-// (DESIGN.md §7). The production kernel (l3_decode_batch) is the fifth bar.
+//   mode 4  one WARP per patch: sequential BD + sequential Paeth (lane 0): modes 4 -> 1 isolate
+//           the pixel-wise BD step from the thread-vs-warp mapping that modes 0 -> 1 also change
+// The paper's baseline uses the ORIGINAL (left/top/top-left) Paeth. Its format variant "L3IP"
+// (reading C16) is decoded by the modes with a sequential Paeth (0, 1, 4); modes 2 and 3
+// (row-parallel Paeth) need the custom-Paeth format and report L3IP images as
+// UNRECOGNIZED_FORMAT. The paper's four bars are: mode 0 on L3IP (Baseline), mode 1 on L3IP
+// (+Pixel-wise BD), mode 2 on L3IF (+Custom Paeth), mode 3 on L3IF (both). The production
+// kernel (l3_decode_batch) is the fifth bar.
 // Valid files only (the ablation reports time, not errors); reads stay inside each unit.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -18,7 +23,7 @@
 
 namespace l3 {
 
-cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s);
+cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_variant);
 
 struct AblParams {
   const uint8_t* src;
@@ -32,15 +37,13 @@ __device__ __forceinline__ uint32_t abl_u32le(const uint8_t* p) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
-// k bits at bit position pos of [data, data+len) MSB-first; 0 past the end.
+// k (<= 8) bits at bit position pos of [data, data+len) MSB-first; 0 past the end. A 16-bit
+// window of the two bytes holding the field (pos & 7 + k <= 15), as plain scalar code would.
 __device__ __forceinline__ uint32_t abl_bits(const uint8_t* data, uint64_t len, uint64_t pos, uint32_t k) {
-  uint32_t v = 0;
-  for (uint32_t i = 0; i < k; i++, pos++) {
-    const uint64_t b = pos >> 3;
-    const uint32_t bit = b < len ? (data[b] >> (7 - (pos & 7))) & 1u : 0u;
-    v = (v << 1) | bit;
-  }
-  return v;
+  const uint64_t b = pos >> 3;
+  const uint32_t hi = b < len ? data[b] : 0u, lo = b + 1 < len ? data[b + 1] : 0u;
+  const uint32_t win = (hi << 8) | lo;
+  return (win >> (16u - (uint32_t)(pos & 7) - k)) & ((1u << k) - 1u);
 }
 
 struct AblUnit {
@@ -48,6 +51,7 @@ struct AblUnit {
   uint64_t len;
   uint8_t* plane;
   uint32_t W, x0, y0, w, h;
+  bool png;   // original-Paeth variant (L3IP)
 };
 
 __device__ __forceinline__ bool abl_unit(const AblParams& p, int img, uint32_t u, AblUnit& U) {
@@ -67,26 +71,55 @@ __device__ __forceinline__ bool abl_unit(const AblParams& p, int img, uint32_t u
   U.w = min(d.N, d.W - U.x0);
   U.h = min(d.N, d.H - U.y0);
   U.plane = p.out + d.out_off + (uint64_t)ch * d.W * d.H;
+  U.png = is_png_variant(file);
   return true;
 }
 
+__device__ __forceinline__ uint64_t abl_image_units(const AblParams& p, int img) {
+  return p.status[img] == L3_OK ? 3ull * p.desc[img].P : 0ull;
+}
+
+// Walks the batch's units in one flat index space (every unit of every image is available to
+// every worker at once); g only grows per worker, so the image cursor advances monotonically.
+struct AblCursor {
+  int img = 0;
+  uint64_t base = 0;
+  __device__ __forceinline__ bool seek(const AblParams& p, uint64_t g, uint32_t& u) {
+    while (img < p.n) {
+      const uint64_t nu = abl_image_units(p, img);
+      if (g < base + nu) break;
+      base += nu;
+      img++;
+    }
+    if (img >= p.n) return false;
+    u = (uint32_t)(g - base);
+    return true;
+  }
+};
+
 // mode 0: one thread per patch, everything sequential
 __global__ void l3_ablation_thread_kernel(AblParams p) {
-  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-  for (int img = 0; img < p.n; img++) {
-    if (p.status[img] != L3_OK) continue;
-    for (uint32_t u = tid; u < 3u * p.desc[img].P; u += nth) {
+  const uint64_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  AblCursor cur;
+  uint32_t u;
+  for (uint64_t g = tid; cur.seek(p, g, u); g += nth) {
+    const int img = cur.img;
+    {
       AblUnit U;
       if (!abl_unit(p, img, u, U)) continue;
       uint64_t pos = 0;
       for (uint32_t r = 0; r < U.h; r++) {
-        const uint32_t k = abl_bits(U.data, U.len, pos, 4), base = abl_bits(U.data, U.len, pos + 4, 8);
+        const uint32_t k = min(abl_bits(U.data, U.len, pos, 4), 8u), base = abl_bits(U.data, U.len, pos + 4, 8);
         pos += 12;
         uint8_t* row = U.plane + (uint64_t)(U.y0 + r) * U.W + U.x0;
         for (uint32_t c = 0; c < U.w; c++, pos += k) {
           const int res = (int)((base + abl_bits(U.data, U.len, pos, k)) & 0xFFu);
           if (r == 0) {
             row[c] = (uint8_t)res;
+          } else if (U.png) {   // left neighbour = the pixel just decoded (row-wise dependency)
+            const uint8_t* up = row - U.W;
+            const int a = c ? row[c - 1] : 0, cc = c ? up[c - 1] : 0;
+            row[c] = (uint8_t)((paeth_png_pred(a, up[c], cc) + res) & 0xFF);
           } else {
             const uint8_t* up = row - U.W;
             const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
@@ -103,16 +136,18 @@ template <bool PAR_BD, bool PAR_PAETH>
 __global__ void l3_ablation_warp_kernel(AblParams p) {
   __shared__ uint8_t res_s[8][256];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   uint8_t* res = res_s[wl];
-  for (int img = 0; img < p.n; img++) {
-    if (p.status[img] != L3_OK) continue;
-    for (uint32_t u = gw; u < 3u * p.desc[img].P; u += nw) {
+  AblCursor cur;
+  uint32_t u;
+  for (uint64_t g = gw; cur.seek(p, g, u); g += nw) {
+    const int img = cur.img;
+    {
       AblUnit U;
       if (!abl_unit(p, img, u, U)) continue;
       uint64_t pos = 0;
       for (uint32_t r = 0; r < U.h; r++) {
-        const uint32_t k = abl_bits(U.data, U.len, pos, 4), base = abl_bits(U.data, U.len, pos + 4, 8);
+        const uint32_t k = min(abl_bits(U.data, U.len, pos, 4), 8u), base = abl_bits(U.data, U.len, pos + 4, 8);
         pos += 12;
         // step 2 of PAPER.md:152: deltas + base
         if (PAR_BD) {
@@ -139,6 +174,9 @@ __global__ void l3_ablation_warp_kernel(AblParams p) {
           for (uint32_t c = 0; c < U.w; c++) {
             if (r == 0) {
               row[c] = res[c];
+            } else if (U.png) {
+              const int a = c ? row[c - 1] : 0, cc = c ? up[c - 1] : 0;
+              row[c] = (uint8_t)((paeth_png_pred(a, up[c], cc) + res[c]) & 0xFF);
             } else {
               const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
               row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res[c]) & 0xFF);
@@ -153,7 +191,7 @@ __global__ void l3_ablation_warp_kernel(AblParams p) {
 }
 
 cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s) {
-  cudaError_t e = launch_parse(a, s);
+  cudaError_t e = launch_parse(a, s, /*accept_variant=*/mode <= 1 || mode == 4);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -168,6 +206,7 @@ cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s) {
   if (mode == 0) l3_ablation_thread_kernel<<<sms * 8, 128, 0, s>>>(p);
   else if (mode == 1) l3_ablation_warp_kernel<true, false><<<sms * 8, 256, 0, s>>>(p);
   else if (mode == 2) l3_ablation_warp_kernel<false, true><<<sms * 8, 256, 0, s>>>(p);
+  else if (mode == 4) l3_ablation_warp_kernel<false, false><<<sms * 8, 256, 0, s>>>(p);
   else l3_ablation_warp_kernel<true, true><<<sms * 8, 256, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -86,6 +86,9 @@ __device__ void block_exclusive_scan2(uint64_t& a, uint64_t& b, uint64_t* sh_a, 
 // Tail zone: images whose units start within the batch's last `tail_units`
 // units (about one per resident warp) are decoded one patch per task on the
 // 4-column path (mode 4), so the end of the persistent kernel is fine-grained.
+// VARIANT (ablation decoders only, reading C16): also accept the original-Paeth
+// format variant "L3IP"; the hot path never instantiates it.
+template <bool VARIANT = false>
 __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc& d) {
   const uint64_t f0 = p.src_offsets[i], f1 = p.src_offsets[i + 1];
   const uint64_t len = f1 > f0 ? f1 - f0 : 0;
@@ -108,7 +111,8 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
   d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)(uint32_t)chh * (uint32_t)cww;
   if (p.crops && (cy < 0 || cx < 0 || chh < 1 || cww < 1 || (int64_t)cy + chh > expH || (int64_t)cx + cww > expW))
     return L3_E_INVALID_ARGUMENT;
-  if (f1 < f0 || len < 4 || __ldg(f) != 'L' || __ldg(f + 1) != '3' || __ldg(f + 2) != 'I' || __ldg(f + 3) != 'F')
+  if (f1 < f0 || len < 4 || __ldg(f) != 'L' || __ldg(f + 1) != '3' || __ldg(f + 2) != 'I' ||
+      (__ldg(f + 3) != 'F' && !(VARIANT && __ldg(f + 3) == 'P')))
     return L3_E_UNRECOGNIZED_FORMAT;
   if (len < 13) return L3_E_CORRUPT_HEADER;
   d.W = ld_u32le(f + 4);
@@ -129,6 +133,7 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
 }
 
 // a1 without the tail zone (kernel variants without the wide path): one pass.
+template <bool VARIANT = false>
 __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
   uint64_t carry0 = 0, carry1 = 0;
   for (int base = 0; base < p.n; base += blockDim.x) {
@@ -136,7 +141,7 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
     uint64_t t0 = 0, t1 = 0;
     if (i < p.n) {
       ImgDesc d;
-      const int st = parse_header(p, i, d);
+      const int st = parse_header<VARIANT>(p, i, d);
       if (st == L3_OK) {
         if (d.mode == 1 || d.mode == 2) {
           d.mode = 4;
@@ -240,9 +245,11 @@ __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b
 }
 
 // Standalone a1 (l3_parse_batch): header validation and work decomposition only.
+// VARIANT: the ablation decoders' parse, which also accepts "L3IP" (reading C16).
+template <bool VARIANT>
 __global__ void __launch_bounds__(1024) l3_parse_kernel(ParseParams p) {
   __shared__ uint64_t sh_a[33], sh_b[33];
-  parse_phase<false>(p, sh_a, sh_b);
+  parse_phase_simple<VARIANT>(p, sh_a, sh_b);
 }
 
 // ============================================================== a2-a7 helpers
@@ -557,8 +564,9 @@ static ParseParams make_parse_params(const l3_decode_args* a) {
   return pp;
 }
 
-cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s) {
-  l3_parse_kernel<<<1, 1024, 0, s>>>(make_parse_params(a));
+cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_variant) {
+  if (accept_variant) l3_parse_kernel<true><<<1, 1024, 0, s>>>(make_parse_params(a));
+  else l3_parse_kernel<false><<<1, 1024, 0, s>>>(make_parse_params(a));
   return cudaGetLastError();
 }
 

@@ -56,6 +56,7 @@ struct EncParams {
   uint8_t* dst;
   uint64_t* dst_offsets;
   EncWs ws;
+  int predictor;        // 0 custom Paeth ("L3IF"), 1 original Paeth ("L3IP", reading C16)
 };
 
 __device__ __forceinline__ int find_image(const uint64_t* prefix, int n, uint64_t u) {
@@ -84,12 +85,14 @@ __device__ __forceinline__ UnitGeom unit_geom(const EncParams& p, const EncDesc&
   return g;
 }
 
-// Residual of column c in row r (row 0 unfiltered, C5).
-__device__ __forceinline__ int residual(const UnitGeom& g, uint32_t r, uint32_t c) {
+// Residual of column c in row r (row 0 unfiltered, C5). The encoder sees the
+// original pixels, so even the original Paeth (left neighbour) is column-parallel here.
+__device__ __forceinline__ int residual(const UnitGeom& g, uint32_t r, uint32_t c, int predictor) {
   const uint8_t* row = g.plane + (uint64_t)(g.y0 + r) * g.W + g.x0;
   const int x = row[c];
   if (r == 0) return x;
   const uint8_t* up = row - g.W;
+  if (predictor) return (x - paeth_png_pred(c ? row[c - 1] : 0, up[c], c ? up[c - 1] : 0)) & 0xFF;
   const int t = up[c];
   const int tl = c > 0 ? up[c - 1] : t;
   const int tr = c + 1 < g.w ? up[c + 1] : t;
@@ -97,10 +100,11 @@ __device__ __forceinline__ int residual(const UnitGeom& g, uint32_t r, uint32_t 
 }
 
 // Row base-delta parameters (readings C2/C6); warp-collective.
-__device__ __forceinline__ void row_kb(const UnitGeom& g, uint32_t r, int lane, int* k, int* base) {
+__device__ __forceinline__ void row_kb(const UnitGeom& g, uint32_t r, int lane, int predictor, int* k,
+                                       int* base) {
   int mn = 1 << 20, mx = -(1 << 20);
   for (uint32_t c = lane; c < g.w; c += 32) {
-    int v = residual(g, r, c);
+    int v = residual(g, r, c, predictor);
     if (r > 0 && v >= 128) v -= 256;
     mn = min(mn, v);
     mx = max(mx, v);
@@ -122,7 +126,7 @@ __global__ void l3_enc_size_kernel(EncParams p) {
     uint64_t bits = 0;
     for (uint32_t r = 0; r < g.h; r++) {
       int k, base;
-      row_kb(g, r, lane, &k, &base);
+      row_kb(g, r, lane, p.predictor, &k, &base);
       bits += 12u + (uint64_t)k * g.w;
     }
     if (lane == 0) p.ws.unit_bytes[u] = (uint32_t)((bits + 7) / 8);
@@ -206,7 +210,7 @@ __global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
     if (lane < 4) file[13 + 4ull * ul + lane] = (uint8_t)(off >> (8 * lane));
     if (ul == 0 && lane < 13) {
       uint8_t b;
-      if (lane < 4) b = (uint8_t)"L3IF"[lane];
+      if (lane < 4) b = (uint8_t)(p.predictor ? "L3IP" : "L3IF")[lane];
       else if (lane < 8) b = (uint8_t)(d.W >> (8 * (lane - 4)));
       else if (lane < 12) b = (uint8_t)(d.H >> (8 * (lane - 8)));
       else b = (uint8_t)d.N;
@@ -218,10 +222,10 @@ __global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
     uint32_t pos = 0;
     for (uint32_t r = 0; r < g.h; r++) {
       int k, base;
-      row_kb(g, r, lane, &k, &base);
+      row_kb(g, r, lane, p.predictor, &k, &base);
       if (lane == 0) put_bits(buf, pos, ((uint32_t)k << 8) | (uint32_t)base, 12);
       for (uint32_t c = lane; c < g.w; c += 32) {
-        const uint32_t delta = (uint32_t)(residual(g, r, c) - base) & 0xFFu;
+        const uint32_t delta = (uint32_t)(residual(g, r, c, p.predictor) - base) & 0xFFu;
         put_bits(buf, pos + 12u + c * (uint32_t)k, delta, (uint32_t)k);
       }
       pos += 12u + (uint32_t)k * g.w;
@@ -290,6 +294,7 @@ l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s) {
   if (!a || a->n < 0 || (a->n > 0 && (!a->images || !a->shapes_host || !a->img_offsets_host || !a->dst ||
                                        !a->dst_offsets || !a->workspace)))
     return L3_E_INVALID_ARGUMENT;
+  if (a->predictor != 0 && a->predictor != 1) return L3_E_INVALID_ARGUMENT;
   if (a->n == 0) return L3_OK;
   EncPlan pl = plan_encode(a->shapes_host, a->n_host, a->n, a->img_offsets_host);
   if (!pl.ok) return L3_E_INVALID_ARGUMENT;
@@ -309,6 +314,7 @@ l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s) {
   p.dst = a->dst;
   p.dst_offsets = a->dst_offsets;
   p.ws = ws;
+  p.predictor = a->predictor;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -171,4 +171,16 @@ __device__ __forceinline__ int paeth_pred(int tl, int t, int tr) {
   return (dtl <= dt && dtl <= dtr) ? tl : p;
 }
 
+// ORIGINAL Paeth predictor (PNG): a = left, b = top, c = top-left;
+// closest of the three to a + b - c, ties a, b, c. Ablation format variant "L3IP"
+// only (reading C16). da = |b - c|, db = |a - c|, dc = |a + b - 2c|.
+__device__ __forceinline__ int paeth_png_pred(int a, int b, int c) {
+  const int da = __usad(b, c, 0), db = __usad(a, c, 0), dc = abs(a + b - 2 * c);
+  if (da <= db && da <= dc) return a;
+  return db <= dc ? b : c;
+}
+
+// File magic "L3IP" (4th byte 'P') selects the original-Paeth variant.
+__device__ __forceinline__ bool is_png_variant(const uint8_t* file) { return file[3] == 'P'; }
+
 }  // namespace l3

@@ -65,6 +65,7 @@ class l3_encode_args(ctypes.Structure):
         ("dst_offsets", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_uint64),
+        ("predictor", ctypes.c_int32),
     ]
 
 
@@ -225,7 +226,7 @@ def l3_encode_workspace_size(shapes_host, n_host=None) -> int:
 
 
 def l3_encode_batch(images: torch.Tensor, img_offsets_host, shapes_host, n_host, dst: torch.Tensor,
-                    dst_offsets: torch.Tensor, workspace: torch.Tensor, stream=None) -> None:
+                    dst_offsets: torch.Tensor, workspace: torch.Tensor, stream=None, predictor: int = 0) -> None:
     import numpy as np
     io = np.ascontiguousarray(img_offsets_host, np.uint64)
     sh = np.ascontiguousarray(shapes_host, np.int32)
@@ -241,4 +242,5 @@ def l3_encode_batch(images: torch.Tensor, img_offsets_host, shapes_host, n_host,
     a.dst_offsets = _dev_ptr(dst_offsets, "dst_offsets", torch.int64)
     a.workspace = _dev_ptr(workspace, "workspace")
     a.workspace_bytes = workspace.numel() * workspace.element_size()
+    a.predictor = predictor
     _check("l3_encode_batch", lib().l3_encode_batch(ctypes.byref(a), _stream(stream)))

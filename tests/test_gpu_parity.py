@@ -374,12 +374,8 @@ def test_crop_skips_patches_outside_the_window():
 
 # ------------------------------------------------------------------ f2: ablation decoders
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
-def test_ablation_decoders_bit_exact(mode):
+def _ablation_decode(files, imgs, mode):
     from paper_2208_08711_b200 import l3
-    imgs = [l3synth.uniform_image(h, w, s) for s, (h, w) in enumerate([(70, 133), (300, 260), (64, 64), (1, 5)])]
-    Ns = [32, 128, 64, 200]
-    files = [l3ref.encode(im, N=N) for im, N in zip(imgs, Ns)]
     src, offs = pack_files(files)
     sizes = [im.size for im in imgs]
     oo = torch.tensor(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64), device="cuda")
@@ -390,8 +386,67 @@ def test_ablation_decoders_bit_exact(mode):
     l3.l3_decode_batch_ablation(a, mode)
     torch.cuda.synchronize()
     flat = out.cpu().numpy()
-    for o, s, im in zip(oo.cpu().numpy(), sizes, imgs):
-        assert np.array_equal(flat[o:o + s].reshape(im.shape), im)
+    got = [flat[o:o + s].reshape(im.shape) for o, s, im in zip(oo.cpu().numpy(), sizes, imgs)]
+    return got, dec.status.cpu().numpy()
+
+
+_ABL_SHAPES = [(70, 133), (300, 260), (64, 64), (1, 5)]
+_ABL_NS = [32, 128, 64, 200]
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+def test_ablation_decoders_bit_exact(mode):
+    imgs = [l3synth.uniform_image(h, w, s) for s, (h, w) in enumerate(_ABL_SHAPES)]
+    files = [l3ref.encode(im, N=N) for im, N in zip(imgs, _ABL_NS)]
+    got, st = _ablation_decode(files, imgs, mode)
+    assert st.tolist() == [0] * len(files)
+    for g, im in zip(got, imgs):
+        assert np.array_equal(g, im)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 4])
+def test_ablation_original_paeth_variant_bit_exact(mode):
+    """The paper's Baseline / +Pixel-wise BD bars decode the original-Paeth variant "L3IP"
+    (reading C16); files from the oracle, mixed with custom-Paeth files in one batch."""
+    imgs = [l3synth.natural(h, w, s, 1.0) if s % 2 else l3synth.uniform_image(h, w, s)
+            for s, (h, w) in enumerate(_ABL_SHAPES + [(129, 257)])]
+    Ns = _ABL_NS + [64]
+    files = [l3ref.encode_variant(im, N=N) if i != 2 else l3ref.encode(im, N=N)
+             for i, (im, N) in enumerate(zip(imgs, Ns))]
+    got, st = _ablation_decode(files, imgs, mode)
+    assert st.tolist() == [0] * len(files)
+    for g, im in zip(got, imgs):
+        assert np.array_equal(g, im)
+
+
+@pytest.mark.parametrize("mode", [2, 3])
+def test_ablation_row_parallel_modes_reject_original_paeth(mode):
+    imgs = [l3synth.uniform_image(h, w, s) for s, (h, w) in enumerate(_ABL_SHAPES[:2])]
+    files = [l3ref.encode_variant(imgs[0], N=32), l3ref.encode(imgs[1], N=128)]
+    got, st = _ablation_decode(files, imgs, mode)
+    assert st.tolist() == [l3ref.E_UNRECOGNIZED_FORMAT, 0]
+    assert np.array_equal(got[1], imgs[1])
+
+
+def test_hot_path_rejects_original_paeth_variant():
+    im = l3synth.uniform_image(40, 50, 1)
+    _, st, bad, *_ = gpu_decode([l3ref.encode_variant(im, N=32), l3ref.encode(im, N=32)], [(40, 50)] * 2)
+    assert st.tolist() == [l3ref.E_UNRECOGNIZED_FORMAT, 0]
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_gpu_encoder_original_paeth_byte_identical(seed):
+    rng = np.random.default_rng(40 + seed)
+    imgs, Ns = [], []
+    for i in range(10):
+        H, W = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        imgs.append(l3synth.natural(H, W, 10 * seed + i, 1.0) if i % 2 else l3synth.uniform_image(H, W, i))
+        Ns.append(int(rng.choice([0, 3, 32, 64, 128, 255])) if H * W < 30000 else 0)
+    src, offs = encode_batch(imgs, patch_sizes=Ns, predictor=1)
+    o = offs.cpu().numpy()
+    buf = src.cpu().numpy()
+    for i, (im, N) in enumerate(zip(imgs, Ns)):
+        assert buf[o[i]:o[i + 1]].tobytes() == l3ref.encode_variant(im, N=N), (i, im.shape, N)
 
 
 # ------------------------------------------------------------------ edge cases: sizes and counts
