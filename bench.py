@@ -293,10 +293,12 @@ def run_ablation(args):
         ("Baseline: orig Paeth seq + BD seq (thread/patch, L3IP)", a_p, 0),
         ("+Pixel-wise BD: orig Paeth seq (warp/patch, L3IP)", a_p, 1),
         ("orig Paeth seq + BD seq (warp/patch lane 0, L3IP)", a_p, 4),
+        ("pixel-wise BD + orig Paeth anti-diagonal wavefront (warp/patch, smem, L3IP)", a_p, 5),
         ("+Custom Paeth: row-parallel, BD seq (warp/patch, L3IF)", a, 2),
         ("+Pixel-wise BD+Custom Paeth (warp/patch, L3IF)", a, 3),
         ("custom Paeth, all seq (thread/patch, L3IF)", a, 0),
         ("custom Paeth seq, pixel-wise BD (warp/patch, L3IF)", a, 1),
+        ("pixel-wise BD + row-parallel custom Paeth (warp/patch, smem, L3IF)", a, 5),
     ]
     res = {nm: round(timed(lambda aa=aa, m=m: l3.l3_decode_batch_ablation(aa, m, stream)), 4) for nm, aa, m in bars}
     res["production (l3_decode_batch, L3IF)"] = round(timed(lambda: l3.l3_decode_batch(a, stream)), 4)

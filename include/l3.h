@@ -150,7 +150,9 @@ int32_t l3_decode_kernels_per_call(void);
  *   mode 2  one warp per patch, sequential base-delta, row-wise parallel Paeth
  *   mode 3  one warp per patch, both parallel (the paper's design, plain scalar code)
  *   mode 4  one warp per patch, sequential base-delta + sequential Paeth (lane 0)
- * Modes 0, 1 and 4 also read the original-Paeth variant "L3IP" (per image, by magic; reading
+ *   mode 5  one warp per patch staged in shared memory: pixel-wise base-delta, then an
+ *           anti-diagonal wavefront (original Paeth) or row-parallel (custom Paeth) reconstruction
+ * Modes 0, 1, 4 and 5 also read the original-Paeth variant "L3IP" (per image, by magic; reading
  * C16), so the paper's Baseline / +Pixel-wise BD bars are modes 0 / 1 on L3IP files. Modes 2
  * and 3 cannot (the left dependency forbids a row-parallel Paeth) and set L3IP images to
  * L3_E_UNRECOGNIZED_FORMAT. Other modes: L3_E_INVALID_ARGUMENT.

@@ -8,8 +8,10 @@
 //   mode 3  one WARP per patch: both (the paper's full design, plain scalar code)
 //   mode 4  one WARP per patch: sequential BD + sequential Paeth (lane 0): modes 4 -> 1 isolate
 //           the pixel-wise BD step from the thread-vs-warp mapping that modes 0 -> 1 also change
+//   mode 5  one WARP per patch in shared memory: pixel-wise BD, then an anti-diagonal wavefront
+//           for the original Paeth or row-parallel for the custom Paeth
 // The paper's baseline uses the ORIGINAL (left/top/top-left) Paeth. Its format variant "L3IP"
-// (reading C16) is decoded by the modes with a sequential Paeth (0, 1, 4); modes 2 and 3
+// (reading C16) is decoded by modes 0, 1, 4 (sequential Paeth) and 5 (wavefront); modes 2 and 3
 // (row-parallel Paeth) need the custom-Paeth format and report L3IP images as
 // UNRECOGNIZED_FORMAT. The paper's four bars are: mode 0 on L3IP (Baseline), mode 1 on L3IP
 // (+Pixel-wise BD), mode 2 on L3IF (+Custom Paeth), mode 3 on L3IF (both). The production
@@ -97,37 +99,109 @@ struct AblCursor {
   }
 };
 
+// Sequential decode of one unit by one thread, straight into the output plane (modes 0, 5 fallback).
+__device__ void abl_seq_unit(const AblUnit& U) {
+  uint64_t pos = 0;
+  for (uint32_t r = 0; r < U.h; r++) {
+    const uint32_t k = min(abl_bits(U.data, U.len, pos, 4), 8u), base = abl_bits(U.data, U.len, pos + 4, 8);
+    pos += 12;
+    uint8_t* row = U.plane + (uint64_t)(U.y0 + r) * U.W + U.x0;
+    for (uint32_t c = 0; c < U.w; c++, pos += k) {
+      const int res = (int)((base + abl_bits(U.data, U.len, pos, k)) & 0xFFu);
+      if (r == 0) {
+        row[c] = (uint8_t)res;
+      } else if (U.png) {   // left neighbour = the pixel just decoded (row-wise dependency)
+        const uint8_t* up = row - U.W;
+        const int a = c ? row[c - 1] : 0, cc = c ? up[c - 1] : 0;
+        row[c] = (uint8_t)((paeth_png_pred(a, up[c], cc) + res) & 0xFF);
+      } else {
+        const uint8_t* up = row - U.W;
+        const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
+        row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res) & 0xFF);
+      }
+    }
+  }
+}
+
 // mode 0: one thread per patch, everything sequential
 __global__ void l3_ablation_thread_kernel(AblParams p) {
   const uint64_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   AblCursor cur;
   uint32_t u;
   for (uint64_t g = tid; cur.seek(p, g, u); g += nth) {
-    const int img = cur.img;
-    {
-      AblUnit U;
-      if (!abl_unit(p, img, u, U)) continue;
+    AblUnit U;
+    if (abl_unit(p, cur.img, u, U)) abl_seq_unit(U);
+  }
+}
+
+// mode 5: one warp per patch, staged in shared memory: row-header chain (lane 0), pixel-wise BD
+// over the whole patch, then the most parallel Paeth order each format allows: an anti-diagonal
+// WAVEFRONT for the original Paeth (pixel (r, c) needs (r, c-1), (r-1, c), (r-1, c-1), all on
+// earlier diagonals r + c; h + w - 2 dependent steps) and row-parallel for the custom Paeth (h - 1
+// steps). Patches above 128 x 128 fall back to lane 0 sequential (N > 128 is outside the policy).
+constexpr uint32_t kWaveCap = 16384, kWaveRows = 128, kWaveWarps = 4;
+constexpr uint32_t kWaveSmem = kWaveWarps * (kWaveCap + kWaveRows * 6);
+
+__global__ void __launch_bounds__(kWaveWarps * 32) l3_ablation_wave_kernel(AblParams p) {
+  extern __shared__ __align__(16) uint8_t wsm[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  uint8_t* px = wsm + wl * kWaveCap;
+  uint32_t* hpos = reinterpret_cast<uint32_t*>(wsm + kWaveWarps * kWaveCap) + wl * kWaveRows;
+  uint8_t* hk = wsm + kWaveWarps * (kWaveCap + 4 * kWaveRows) + wl * kWaveRows;
+  uint8_t* hb = hk + kWaveWarps * kWaveRows;
+  const uint64_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  AblCursor cur;
+  uint32_t u;
+  for (uint64_t g = gw; cur.seek(p, g, u); g += nw) {
+    AblUnit U;
+    if (!abl_unit(p, cur.img, u, U)) continue;
+    const uint32_t w = U.w, h = U.h;
+    if (h > kWaveRows || w * h > kWaveCap) {
+      if (lane == 0) abl_seq_unit(U);
+      __syncwarp();
+      continue;
+    }
+    if (lane == 0) {   // a3: the row-header chain is serial by construction
       uint64_t pos = 0;
-      for (uint32_t r = 0; r < U.h; r++) {
-        const uint32_t k = min(abl_bits(U.data, U.len, pos, 4), 8u), base = abl_bits(U.data, U.len, pos + 4, 8);
-        pos += 12;
-        uint8_t* row = U.plane + (uint64_t)(U.y0 + r) * U.W + U.x0;
-        for (uint32_t c = 0; c < U.w; c++, pos += k) {
-          const int res = (int)((base + abl_bits(U.data, U.len, pos, k)) & 0xFFu);
-          if (r == 0) {
-            row[c] = (uint8_t)res;
-          } else if (U.png) {   // left neighbour = the pixel just decoded (row-wise dependency)
-            const uint8_t* up = row - U.W;
-            const int a = c ? row[c - 1] : 0, cc = c ? up[c - 1] : 0;
-            row[c] = (uint8_t)((paeth_png_pred(a, up[c], cc) + res) & 0xFF);
-          } else {
-            const uint8_t* up = row - U.W;
-            const int t = up[c], tl = c ? up[c - 1] : t, tr = (c + 1 < U.w) ? up[c + 1] : t;
-            row[c] = (uint8_t)((paeth_pred(tl, t, tr) + res) & 0xFF);
-          }
-        }
+      for (uint32_t r = 0; r < h; r++) {
+        const uint32_t k = min(abl_bits(U.data, U.len, pos, 4), 8u);
+        hk[r] = (uint8_t)k;
+        hb[r] = (uint8_t)abl_bits(U.data, U.len, pos + 4, 8);
+        hpos[r] = (uint32_t)(pos + 12);
+        pos += 12 + (uint64_t)k * w;
       }
     }
+    __syncwarp();
+    for (uint32_t i = lane; i < w * h; i += 32) {   // a4 for every pixel of the patch
+      const uint32_t r = i / w, c = i - r * w, k = hk[r];
+      px[i] = (uint8_t)((hb[r] + abl_bits(U.data, U.len, (uint64_t)hpos[r] + (uint64_t)c * k, k)) & 0xFFu);
+    }
+    __syncwarp();
+    if (U.png) {
+      for (uint32_t d = 1; d + 1 < h + w; d++) {
+        const uint32_t r0 = d + 1 > w ? d + 1 - w : 1u, r1 = min(d, h - 1);
+        for (uint32_t r = max(r0, 1u) + lane; r <= r1; r += 32) {
+          const uint32_t c = d - r, i = r * w + c;
+          const int a = c ? px[i - 1] : 0, b = px[i - w], cc = c ? px[i - w - 1] : 0;
+          px[i] = (uint8_t)((paeth_png_pred(a, b, cc) + px[i]) & 0xFF);
+        }
+        __syncwarp();
+      }
+    } else {
+      for (uint32_t r = 1; r < h; r++) {
+        for (uint32_t c = lane; c < w; c += 32) {
+          const uint32_t i = r * w + c;
+          const int t = px[i - w], tl = c ? px[i - w - 1] : t, tr = (c + 1 < w) ? px[i - w + 1] : t;
+          px[i] = (uint8_t)((paeth_pred(tl, t, tr) + px[i]) & 0xFF);
+        }
+        __syncwarp();
+      }
+    }
+    for (uint32_t i = lane; i < w * h; i += 32) {
+      const uint32_t r = i / w, c = i - r * w;
+      U.plane[(uint64_t)(U.y0 + r) * U.W + U.x0 + c] = px[i];
+    }
+    __syncwarp();
   }
 }
 
@@ -191,7 +265,7 @@ __global__ void l3_ablation_warp_kernel(AblParams p) {
 }
 
 cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s) {
-  cudaError_t e = launch_parse(a, s, /*accept_variant=*/mode <= 1 || mode == 4);
+  cudaError_t e = launch_parse(a, s, /*accept_variant=*/mode <= 1 || mode >= 4);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -207,7 +281,12 @@ cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s) {
   else if (mode == 1) l3_ablation_warp_kernel<true, false><<<sms * 8, 256, 0, s>>>(p);
   else if (mode == 2) l3_ablation_warp_kernel<false, true><<<sms * 8, 256, 0, s>>>(p);
   else if (mode == 4) l3_ablation_warp_kernel<false, false><<<sms * 8, 256, 0, s>>>(p);
-  else l3_ablation_warp_kernel<true, true><<<sms * 8, 256, 0, s>>>(p);
+  else if (mode == 5) {
+    e = cudaFuncSetAttribute(l3_ablation_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWaveSmem);
+    if (e != cudaSuccess) return e;
+    l3_ablation_wave_kernel<<<sms * 3, kWaveWarps * 32, kWaveSmem, s>>>(p);
+  }
+  else if (mode == 3) l3_ablation_warp_kernel<true, true><<<sms * 8, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

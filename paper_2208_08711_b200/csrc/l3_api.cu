@@ -64,7 +64,7 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* a, const void* host_src, 
 l3_status_t l3_decode_batch_ablation(const l3_decode_args* a, int32_t mode, l3_stream_t stream) {
   l3_status_t st = check_decode_args(a);
   if (st != L3_OK || a->n == 0) return st;
-  if (mode < 0 || mode > 4 || a->out_kind != L3_OUT_U8 || a->crops) return L3_E_INVALID_ARGUMENT;
+  if (mode < 0 || mode > 5 || a->out_kind != L3_OUT_U8 || a->crops) return L3_E_INVALID_ARGUMENT;
   return l3::launch_ablation(a, mode, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 

@@ -394,7 +394,7 @@ _ABL_SHAPES = [(70, 133), (300, 260), (64, 64), (1, 5)]
 _ABL_NS = [32, 128, 64, 200]
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 def test_ablation_decoders_bit_exact(mode):
     imgs = [l3synth.uniform_image(h, w, s) for s, (h, w) in enumerate(_ABL_SHAPES)]
     files = [l3ref.encode(im, N=N) for im, N in zip(imgs, _ABL_NS)]
@@ -404,7 +404,7 @@ def test_ablation_decoders_bit_exact(mode):
         assert np.array_equal(g, im)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 4])
+@pytest.mark.parametrize("mode", [0, 1, 4, 5])
 def test_ablation_original_paeth_variant_bit_exact(mode):
     """The paper's Baseline / +Pixel-wise BD bars decode the original-Paeth variant "L3IP"
     (reading C16); files from the oracle, mixed with custom-Paeth files in one batch."""
