@@ -47,6 +47,7 @@ def parse_args():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for the barrier / max-over-ranks plumbing (gloo: single-GPU tests)")
     ap.add_argument("--crop", default=None, help="HxW: f3 partial-decode bench (random window + flip per image)")
+    ap.add_argument("--layout", default="chw", choices=["chw", "hwc"], help="--crop bench: window output layout")
     ap.add_argument("--ablation", action="store_true",
                     help="f2: time the paper's Fig. 10 decoder variants (u8) on the config, vs the production kernel")
     ap.add_argument("--share-device", action="store_true",
@@ -224,8 +225,9 @@ def run_crop(args):
     dec = BatchDecoder(n)
     stream = torch.cuda.Stream()
     from paper_2208_08711_b200 import l3
-    a_c = [dec.args(x, offs, shapes, out_c, scale=scale, bias=bias, crops=crops_t) for x in srcs]
+    a_c = [dec.args(x, offs, shapes, out_c, scale=scale, bias=bias, crops=crops_t, layout=args.layout) for x in srcs]
     a_f = [dec.args(x, offs, shapes, out_f, out_offsets=oo, scale=scale, bias=bias) for x in srcs]
+    a_h = [dec.args(x, offs, shapes, out_f, out_offsets=oo, scale=scale, bias=bias, layout="hwc") for x in srcs]
 
     def timed(alist):
         for i in range(args.warmup):
@@ -238,14 +240,15 @@ def run_crop(args):
         e1.synchronize()
         assert bool((dec.status[:n] == 0).all())
         return e0.elapsed_time(e1) / args.steps
-    ms_c, ms_f = timed(a_c), timed(a_f)
+    ms_c, ms_f, ms_h = timed(a_c), timed(a_f), timed(a_h)
     win_px = n * ch_ * cw_
     line = {"metric": "decoded window Mpixel/s (partial decode, f3)", "value": round(win_px / (ms_c / 1e3) / 1e6, 3),
             "unit": "Mpixel/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_c, 4), "higher_is_better": True, "dtype": "u8", "data": "synthetic",
             "config": {"workload": args.config + f": random {ch_}x{cw_} window + random flip per image, out "
-                       + out_kind, "batch": n},
+                       + out_kind + " " + args.layout.upper(), "batch": n},
             "ms_full_decode": round(ms_f, 4), "speedup_vs_full_decode": round(ms_f / ms_c, 3),
+            "ms_full_decode_hwc": round(ms_h, 4),
             "window_fraction_of_pixels": round(win_px / float((shapes_np[:, 0] * shapes_np[:, 1]).sum()), 4)}
     print(json.dumps(line), flush=True)
 

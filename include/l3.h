@@ -70,26 +70,31 @@ typedef void* l3_stream_t;
  *   shapes       device, n x {H, W} int32: the caller's expected shape of image i;
  *                a header that disagrees is L3_E_CORRUPT_HEADER.
  *   out          device: decoded output (u8 or f32 elements per out_kind).
- *   out_offsets  device, n uint64 ELEMENT offsets of image i's [3,H,W] block, or
- *                NULL: image i starts at element i*3*H_i*W_i (dense [n,3,H,W]
- *                when every shape is equal).
+ *   out_offsets  device, n uint64 ELEMENT offsets of image i's [3,H,W] block (or its
+ *                [H,W,3] block with L3_DECODE_LAYOUT_HWC), or NULL: image i starts at
+ *                element i*3*H_i*W_i (dense [n,3,H,W] / [n,H,W,3] when every shape is equal).
  *   scale, bias  F32 only: per channel (R, G, B).
  *   status       device, n int32 (l3_status_t), written by the call.
  *   bad_unit     device, n int32 or NULL: first failing unit ch*P + p, else -1.
  *   workspace    device, >= l3_decode_workspace_size(n) bytes, 256-byte aligned,
  *                zero-filled before first use (see l3_decode_batch).
- *   flags        L3_DECODE_HINT_* performance hints (0 = none).
+ *   flags        L3_DECODE_HINT_* performance hints and L3_DECODE_LAYOUT_HWC (0 = none).
  *   crops        optional: image i is decoded only inside the window rows [y, y+h) x cols
  *                [x, x+w) (flip != 0: mirrored left-right) into a [3, h, w] block (dense:
  *                element i*3*h*w). Only the patches the window touches are read and decoded
  *                (patches are independently addressable); status then covers
  *                the header and those patches. A window outside the image is
- *                L3_E_INVALID_ARGUMENT in status[i].
+ *                L3_E_INVALID_ARGUMENT in status[i]. With L3_DECODE_LAYOUT_HWC the block
+ *                is [h, w, 3].
  */
 /* l3_decode_args.flags */
 #define L3_DECODE_HINT_WIDE 1u   /* u8 out: most files use 33 <= N <= 128 (e.g. policy N = 128 for
                                     >= FHD images): pick the 8-column-per-lane kernel variant.
                                     A performance hint only; every file decodes correctly either way. */
+#define L3_DECODE_LAYOUT_HWC 2u  /* f3: interleaved output, element (y, x, c) of image i
+                                    at out_offsets[i] + (y * W + x) * 3 + c (W = window width with
+                                    crops), u8 or f32 per out_kind; the channel planes of the file
+                                     are interleaved in the store epilogue. */
 
 typedef struct {
   const uint8_t* src;

@@ -60,22 +60,26 @@ class BatchDecoder:
         self.bad_unit = torch.empty(max_n, dtype=torch.int32, device=self.device)
 
     def args(self, src, src_offsets, shapes, out, *, out_offsets=None, scale=(1.0, 1.0, 1.0),
-             bias=(0.0, 0.0, 0.0), wide=False, crops=None):
+             bias=(0.0, 0.0, 0.0), wide=False, crops=None, layout="chw"):
         n = int(shapes.shape[0])
+        if layout not in ("chw", "hwc"):
+            raise ValueError(f"layout must be 'chw' or 'hwc', got {layout!r}")
+        flags = (l3.L3_DECODE_HINT_WIDE if wide else 0) | (l3.L3_DECODE_LAYOUT_HWC if layout == "hwc" else 0)
         if n > self.max_n:
             raise ValueError(f"batch of {n} > max_n={self.max_n}")
         return l3.make_decode_args(src, src_offsets, shapes, out, self.status[:n], self.workspace,
                                    out_offsets=out_offsets, bad_unit=self.bad_unit[:n], scale=scale, bias=bias,
-                                   flags=l3.L3_DECODE_HINT_WIDE if wide else 0, crops=crops)
+                                   flags=flags, crops=crops)
 
     def decode(self, src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor,
                out: torch.Tensor, *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0),
-               stream=None, wide=False, crops=None):
+               stream=None, wide=False, crops=None, layout="chw"):
         """Enqueue one batch decode on `stream`; returns (status, bad_unit) device views.
         wide: performance hint for u8 batches of large images (policy N = 128), see l3.h.
-        crops: optional int32 [n, 5] device tensor {y, x, h, w, flip}: decode only that window."""
+        crops: optional int32 [n, 5] device tensor {y, x, h, w, flip}: decode only that window.
+        layout: "chw" (planar, default) or "hwc" (interleaved, L3_DECODE_LAYOUT_HWC)."""
         a = self.args(src, src_offsets, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide,
-                      crops=crops)
+                      crops=crops, layout=layout)
         l3.l3_decode_batch(a, stream)
         n = int(shapes.shape[0])
         return self.status[:n], self.bad_unit[:n]

@@ -36,6 +36,7 @@ struct ParseParams {
   WsView ws;
   uint32_t tail_units;   // the last tail_units units of the batch run as 1-patch tasks (mode 4)
   uint32_t wide;         // 1: 33 <= N <= 128 may use the wide 8-column path (u8 out); 0: always mode 4
+  uint32_t hwc;          // 1: interleaved [h, w, 3] output (augment variant only, f3)
 };
 
 __device__ __forceinline__ uint32_t ld_u32le(const uint8_t* p) {
@@ -88,7 +89,8 @@ __device__ void block_exclusive_scan2(uint64_t& a, uint64_t& b, uint64_t* sh_a, 
 // 4-column path (mode 4), so the end of the persistent kernel is fine-grained.
 // VARIANT (ablation decoders only, reading C16): also accept the original-Paeth
 // format variant "L3IP"; the hot path never instantiates it.
-template <bool VARIANT = false>
+// AUG: the augment (crop / flip / HWC) kernel variant, the only reader of the layout bit.
+template <bool VARIANT = false, bool AUG = false>
 __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc& d) {
   const uint64_t f0 = p.src_offsets[i], f1 = p.src_offsets[i + 1];
   const uint64_t len = f1 > f0 ? f1 - f0 : 0;
@@ -107,7 +109,7 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
   d.cx = (uint32_t)cx;
   d.ch = (uint32_t)chh;
   d.cw = (uint32_t)cww;
-  d.flip = flip ? 1u : 0u;
+  d.flip = (flip ? 1u : 0u) | ((AUG && p.hwc) ? 2u : 0u);   // bit 0: flip, bit 1: HWC layout
   d.out_off = p.out_offsets ? p.out_offsets[i] : (uint64_t)i * 3ull * (uint64_t)(uint32_t)chh * (uint32_t)cww;
   if (p.crops && (cy < 0 || cx < 0 || chh < 1 || cww < 1 || (int64_t)cy + chh > expH || (int64_t)cx + cww > expW))
     return L3_E_INVALID_ARGUMENT;
@@ -133,7 +135,8 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
 }
 
 // a1 without the tail zone (kernel variants without the wide path): one pass.
-template <bool VARIANT = false>
+// HWCK: the HWC kernel's decomposition: one task per (image, patch) for N <= 128 (mode 5).
+template <bool VARIANT = false, bool AUG = false, bool HWCK = false>
 __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
   uint64_t carry0 = 0, carry1 = 0;
   for (int base = 0; base < p.n; base += blockDim.x) {
@@ -141,7 +144,7 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
     uint64_t t0 = 0, t1 = 0;
     if (i < p.n) {
       ImgDesc d;
-      const int st = parse_header<VARIANT>(p, i, d);
+      const int st = parse_header<VARIANT, AUG>(p, i, d);
       if (st == L3_OK) {
         if (d.mode == 1 || d.mode == 2) {
           d.mode = 4;
@@ -149,6 +152,10 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
           d.G = 1;
         }
         d.tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
+        if (HWCK && d.mode != 3) {
+          d.mode = 5;
+          d.tasks = d.P;
+        }
         if (d.mode != 3) t0 = d.tasks; else t1 = d.tasks;
       } else {
         d.tasks = 0;
@@ -173,10 +180,10 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
   }
 }
 
-template <bool WIDE>
+template <bool WIDE, bool AUG>
 __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
   if (!WIDE) {   // every 33 <= N <= 128 image runs as 1-patch tasks (mode 4)
-    parse_phase_simple(p, sh_a, sh_b);
+    parse_phase_simple<false, AUG>(p, sh_a, sh_b);
     return;
   }
   // pass 1 (wide path only): total class-0 units, for the tail zone
@@ -249,7 +256,7 @@ __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b
 template <bool VARIANT>
 __global__ void __launch_bounds__(1024) l3_parse_kernel(ParseParams p) {
   __shared__ uint64_t sh_a[33], sh_b[33];
-  parse_phase_simple<VARIANT>(p, sh_a, sh_b);
+  parse_phase_simple<VARIANT, true>(p, sh_a, sh_b);
 }
 
 // ============================================================== a2-a7 helpers
@@ -307,7 +314,7 @@ struct GenericArgs {
   float scale[3], bias[3];
 };
 
-template <bool F32, bool CROP>
+template <bool F32, bool CROP, bool HWC = false>   // HWC: window written interleaved [h, w, 3]
 __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uint8_t* ring8, uint64_t* bars,
                                               uint32_t phase_bits) {
   constexpr int MAXCH = 2;
@@ -360,7 +367,9 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
   }
   __syncwarp();
   const uint32_t seg_bit0 = bitpos;
-  const uint64_t plane = CROP ? d.out_off + (uint64_t)ch * d.ch * d.cw : d.out_off + (uint64_t)ch * d.W * d.H;
+  // CROP (augment) variant: element (y, x) of channel ch at plane + (y * cw + x) * cs
+  const uint64_t plane = CROP ? d.out_off + (HWC ? (uint64_t)ch : (uint64_t)ch * d.ch * d.cw)
+                              : d.out_off + (uint64_t)ch * d.W * d.H;
   const float sc = F32 ? (ch == 0 ? ga.scale[0] : (ch == 1 ? ga.scale[1] : ga.scale[2])) : 0.f;
   const float bi = F32 ? (ch == 0 ? ga.bias[0] : (ch == 1 ? ga.bias[1] : ga.bias[2])) : 0.f;
   int prev[MAXCH][4];
@@ -454,7 +463,8 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
           if (CROP) {
             const int32_t cj = (int32_t)(x0 + c + s) - (int32_t)d.cx;
             if ((uint32_t)cj >= d.cw) continue;
-            e = row_off + (d.flip ? d.cw - 1u - (uint32_t)cj : (uint32_t)cj);
+            if (HWC) e = plane + ((uint64_t)(uint32_t)ri * d.cw + ((d.flip & 1u) ? d.cw - 1u - (uint32_t)cj : (uint32_t)cj)) * 3u;
+            else e = row_off + (d.flip ? d.cw - 1u - (uint32_t)cj : (uint32_t)cj);
           }
           if (F32) reinterpret_cast<float*>(ga.out)[e] = fmaf((float)pix[q][s], sc, bi);
           else reinterpret_cast<uint8_t*>(ga.out)[e] = (uint8_t)pix[q][s];
@@ -494,6 +504,7 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
 }  // namespace l3
 
 #include "l3_decode_fast.cuh"
+#include "l3_decode_hwc.cuh"
 
 namespace l3 {
 
@@ -519,15 +530,24 @@ cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
 
 // ============================================================== host launch
 static int g_sm_count = 0;
-static int g_occ[6] = {0, 0, 0, 0, 0, 0};   // f32, u8 narrow, u8 wide, f32 crop, u8 crop, f32 wide
+// f32, u8 narrow, u8 wide, f32 crop, u8 crop, f32 wide, f32 HWC tile, u8 HWC tile, f32 crop HWC, u8 crop HWC
+static int g_occ[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
-template <bool F32, bool WIDE, bool CROP>
+template <bool F32, bool WIDE, bool CROP, bool HWC = false>
 static int fused_occupancy() {
   int occ = 0;
-  cudaFuncSetAttribute(l3_decode_kernel<F32, WIDE, CROP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(l3_decode_kernel<F32, WIDE, CROP, HWC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)fast_smem_bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32, WIDE, CROP>, kWarpsPerCta * 32,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_kernel<F32, WIDE, CROP, HWC>, kWarpsPerCta * 32,
                                                 fast_smem_bytes());
+  return occ > 0 ? occ : 1;
+}
+
+template <bool F32>
+static int hwc_occupancy() {
+  int occ = 0;
+  cudaFuncSetAttribute(l3_decode_hwc_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hwc_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_hwc_kernel<F32>, kHwcWarps * 32, hwc_smem_bytes());
   return occ > 0 ? occ : 1;
 }
 
@@ -544,6 +564,10 @@ cudaError_t ensure_device_info() {
     g_occ[3] = fused_occupancy<true, false, true>();
     g_occ[4] = fused_occupancy<false, false, true>();
     g_occ[5] = fused_occupancy<true, true, false>();
+    g_occ[6] = hwc_occupancy<true>();
+    g_occ[7] = hwc_occupancy<false>();
+    g_occ[8] = fused_occupancy<true, false, true, true>();
+    g_occ[9] = fused_occupancy<false, false, true, true>();
   }
   return cudaSuccess;
 }
@@ -561,6 +585,7 @@ static ParseParams make_parse_params(const l3_decode_args* a) {
   pp.ws = WsView::at(a->workspace, a->n);
   pp.tail_units = 0;
   pp.wide = 0;
+  pp.hwc = (a->flags & L3_DECODE_LAYOUT_HWC) ? 1u : 0u;
   return pp;
 }
 
@@ -583,9 +608,18 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   }
   dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
+  // f3: full-image HWC -> the tile kernel; crop window / flip (CHW or HWC) -> the augment variant
+  if ((a->flags & L3_DECODE_LAYOUT_HWC) && a->crops == nullptr) {
+    const int v = f32 ? 6 : 7;
+    const int grid = g_sm_count * g_occ[v];
+    if (f32) l3_decode_hwc_kernel<true><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
+    else l3_decode_hwc_kernel<false><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
+    return cudaGetLastError();
+  }
   const bool crop = a->crops != nullptr;
+  const bool crop_hwc = crop && (a->flags & L3_DECODE_LAYOUT_HWC);
   const bool wide = !crop && (a->flags & L3_DECODE_HINT_WIDE);
-  const int variant = crop ? (f32 ? 3 : 4) : (f32 ? (wide ? 5 : 0) : (wide ? 2 : 1));
+  const int variant = crop_hwc ? (f32 ? 8 : 9) : crop ? (f32 ? 3 : 4) : (f32 ? (wide ? 5 : 0) : (wide ? 2 : 1));
   int ctas = g_occ[variant];
   if (const char* e = getenv("L3_DEV_CTAS_PER_SM")) {   // dev-only A/B of the persistent grid
     const int v = atoi(e);
@@ -602,6 +636,8 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
     case 2: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
     case 3: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
     case 4: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
+    case 8: l3_decode_kernel<true, false, true, true><<<grid, B, smem, s>>>(dp); break;
+    case 9: l3_decode_kernel<false, false, true, true><<<grid, B, smem, s>>>(dp); break;
     default: l3_decode_kernel<true, true, false><<<grid, B, smem, s>>>(dp); break;
   }
   return cudaGetLastError();

@@ -38,8 +38,11 @@ __host__ __device__ constexpr size_t fast_smem_bytes() {
 // 32 stream bits at unwrapped ring bit position `bit` (MSB-first, reading C8).
 // Ring words are byte-swapped once when their chunk lands (swap_words), so a
 // word's bit 31 is the first stream bit of that word.
+// SLOTS: ring size in kSlotBytes slots (the HWC kernel runs 4-slot rings, three per warp).
+template <int SLOTS = kSlots>
 __device__ __forceinline__ uint32_t rbits(const uint8_t* ring, uint32_t bit) {
-  const uint32_t* p = reinterpret_cast<const uint32_t*>(ring + ((bit >> 3) & (uint32_t)(kRingBytes - 4)));
+  const uint32_t* p =
+      reinterpret_cast<const uint32_t*>(ring + ((bit >> 3) & (uint32_t)(SLOTS * kSlotBytes - 4)));
   const uint32_t hi = p[0];
   const uint32_t lo = p[1];   // at the ring end this is the mirror of word 0
   uint32_t d;
@@ -68,37 +71,40 @@ struct StreamState {
   uint32_t landed_end;  // A-relative bytes known to be resident (0xFFFFFFFF = all)
 };
 
+template <int SLOTS = kSlots>
 __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                              uint64_t* bars, int lane) {
   const uint32_t c = s.issued;
   const uint64_t ca = s.A + (uint64_t)c * kSlotBytes;
   const uint64_t cb = min(ca + kSlotBytes, s.B);
-  stage_range(src, ca, cb, lim, s.stage_end, ring + (c % kSlots) * kSlotBytes, &bars[c % kSlots], lane == 0, lane,
+  stage_range(src, ca, cb, lim, s.stage_end, ring + (c % SLOTS) * kSlotBytes, &bars[c % SLOTS], lane == 0, lane,
               32);
   s.issued = c + 1;
 }
 
 // Slow path of the per-row ring test: refill consumed slots, then wait until
 // `need` A-relative bytes are resident. Warp-collective.
+template <int SLOTS = kSlots>
 __device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                             uint64_t* bars, uint32_t& phase_bits, uint32_t consumed_byte,
                                             uint32_t need, int lane) {
   const uint32_t consumed = consumed_byte / kSlotBytes;
-  if (s.issued < s.nchunks && s.issued < consumed + kSlots) {
+  if (s.issued < s.nchunks && s.issued < consumed + SLOTS) {
     __syncwarp();
     fence_proxy_async_smem();
-    while (s.issued < s.nchunks && s.issued < consumed + kSlots) stream_issue(src, lim, s, ring, bars, lane);
+    while (s.issued < s.nchunks && s.issued < consumed + SLOTS) stream_issue<SLOTS>(src, lim, s, ring, bars, lane);
     __syncwarp();
   }
   while (s.landed < s.issued && (uint64_t)s.landed * kSlotBytes < need) {
-    const uint32_t sl = s.landed % kSlots;
+    const uint32_t sl = s.landed % SLOTS;
     mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
     phase_bits ^= 1u << sl;
     __syncwarp();
     swap_words(ring, sl * kSlotBytes, (sl + 1) * kSlotBytes, lane, 32);
     __syncwarp();
     if (sl == 0) {   // keep the 16-byte mirror of word 0.. after the ring end current
-      if (lane < 4) reinterpret_cast<uint32_t*>(ring + kRingBytes)[lane] = reinterpret_cast<uint32_t*>(ring)[lane];
+      if (lane < 4)
+        reinterpret_cast<uint32_t*>(ring + SLOTS * kSlotBytes)[lane] = reinterpret_cast<uint32_t*>(ring)[lane];
       __syncwarp();
     }
     s.landed++;
@@ -208,8 +214,8 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
   }
 }
 
-// f3: store the lane's 4 samples into a cropped (optionally flipped) window.
-template <bool F32>
+// f3: store the lane's 4 samples into a cropped (optionally flipped) window, planar or HWC.
+template <bool F32, bool HWC>
 __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi,
                                             bool pred) {
   if (!pred || (uint32_t)s.ri >= s.chh) return;
@@ -219,7 +225,7 @@ __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint
   for (int t = 0; t < 4; t++) {
     const int32_t c = s.cj0 + t;
     if (s.j4 + t < s.w && (uint32_t)c < s.cw) {
-      const uint64_t e = row + (s.flip ? (s.cw - 1u - (uint32_t)c) : (uint32_t)c);
+      const uint64_t e = (row + (s.flip ? (s.cw - 1u - (uint32_t)c) : (uint32_t)c)) * (HWC ? 3u : 1u);
       if (F32) reinterpret_cast<float*>(s.optr)[e] = fmaf((float)x[t], sc, bi);
       else s.optr[e] = (uint8_t)x[t];
     }
@@ -234,7 +240,9 @@ __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint
 // that case (reads stay inside the ring, writes inside the patch) and the
 // exact first error is re-derived after the patch (unit_first_error).
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
-template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP>
+// STORE = false (HWC kernel): the row's pixels are left in s.A / s.B for an interleaving store.
+template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP, bool STORE = true, int SLOTS = kSlots,
+          bool HWC = false>
 __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
   const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
@@ -244,9 +252,9 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   const uint32_t rowbits = 12u + k * s.w;
   const bool live = GUARD ? (r < s.h) : true;
   const uint32_t nbp = s.bp + rowbits;
-  const uint32_t raw_next = rbits(ring, nbp);           // next row's header, fetched early
+  const uint32_t raw_next = rbits<SLOTS>(ring, nbp);    // next row's header, fetched early
   // a4: pixel-wise delta unpack (PAPER.md:152 step 2, :187): field = 4 k-bit deltas, MSB-first
-  const uint32_t field = rbits(ring, s.bp + 12u + s.j4 * k);
+  const uint32_t field = rbits<SLOTS>(ring, s.bp + 12u + s.j4 * k);
   const uint32_t sh = 32u - k;
   const uint32_t pk = shl_c(1u, k);
   const uint32_t d0 = shr_c(field, sh);
@@ -277,8 +285,12 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
   }
   // a6: store (u8 planar, or fused cast + normalise)
-  if (CROP) store4_crop<F32>(s, xA, xB, sc, bi, live && s.valid);
-  else store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
+  if (!STORE) {
+  } else if (CROP) {
+    store4_crop<F32, HWC>(s, xA, xB, sc, bi, live && s.valid);
+  } else {
+    store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
+  }
   s.A = xA;
   s.B = xB;
   if (live) {
@@ -286,11 +298,15 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     s.bp = nbp;
     s.raw = raw_next;
   }
-  if (CROP) s.ri++;
-  else s.optr += s.pitch;
+  if (!STORE) {
+  } else if (CROP) {
+    s.ri++;
+  } else {
+    s.optr += s.pitch;
+  }
 }
 
-template <bool F32, bool FAST, bool STREAM, bool CROP>
+template <bool F32, bool FAST, bool STREAM, bool CROP, bool HWC>
 __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uint32_t hmax, uint32_t Lw, float sc,
                                                  float bi, uint32_t K, const uint8_t* src, uint64_t lim,
                                                  StreamState& st, uint64_t* bars, uint32_t& phase_bits,
@@ -299,18 +315,18 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
     stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
   s.raw = rbits(ring, s.bp);
-  decode_row<true, F32, FAST, GUARD, CROP>(s, ring, 0, Lw, sc, bi, K);
+  decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r, Lw, sc, bi, K);
-    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r + 1, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r, Lw, sc, bi, K);
   }
 }
 
@@ -343,7 +359,8 @@ namespace l3 {
 // fits 80 registers = 6 CTAs / 24 warps per SM (fp32 out, and u8 batches of
 // small patches); WIDE (u8 out, L3_DECODE_HINT_WIDE) carries the 8-column path
 // for 33 <= N <= 128 and runs at 4 CTAs per SM.
-template <bool F32, bool WIDE, bool CROP>
+// HWC (with CROP only): the augment variant writes the window interleaved [h, w, 3].
+template <bool F32, bool WIDE, bool CROP, bool HWC = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -364,7 +381,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
   // publishes the work decomposition; the other CTAs wait on the ready flag
   // (CTA 0 is dispatched first, so the wait cannot starve it).
   if (blockIdx.x == 0) {
-    parse_phase<WIDE>(p.pp, sh_a, sh_b);
+    parse_phase<WIDE, HWC>(p.pp, sh_a, sh_b);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
@@ -453,14 +470,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     s.kacc = 0;
     s.A = s.B = 0;
     const uint32_t esz = F32 ? 4u : 1u;
-    if (CROP) {
-      s.optr = reinterpret_cast<uint8_t*>(p.out) + (d.out_off + (uint64_t)ch * d.ch * d.cw) * esz;
+    if (CROP) {   // augment variant (f3): window, flip; planar, or HWC (interleaved channels)
+      s.optr = reinterpret_cast<uint8_t*>(p.out) +
+               (d.out_off + (HWC ? (uint64_t)ch : (uint64_t)ch * d.ch * d.cw)) * esz;
       s.pitch = 0;
       s.ri = (int32_t)y0 - (int32_t)d.cy;
       s.cj0 = (int32_t)(x0 + s.j4) - (int32_t)d.cx;
       s.cw = d.cw;
       s.chh = d.ch;
-      s.flip = d.flip != 0;
+      s.flip = HWC ? (d.flip & 1u) != 0 : d.flip != 0;
     } else {
       const uint64_t elem = d.out_off + (uint64_t)ch * d.W * d.H + (uint64_t)y0 * d.W + x0 + s.j4;
       s.optr = reinterpret_cast<uint8_t*>(p.out) + elem * esz;
@@ -528,14 +546,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     if (hmax > 0) {
       if (stream) {
         if (fast)
-          decode_unit_rows<F32, true, true, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, true, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       } else {
         if (fast)
-          decode_unit_rows<F32, true, false, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, true, false, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
         else
-          decode_unit_rows<F32, false, false, CROP>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          decode_unit_rows<F32, false, false, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       }
     }
     const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
@@ -576,7 +594,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
       if (lane == 0) t1 = atomicAdd(&head->next_task[1], 1ull);
       t1 = __shfl_sync(0xffffffffu, t1, 0);
       if (t1 >= total1) break;
-      phase_bits = generic_task<F32, CROP>(ga, t1, ring, bars, phase_bits);
+      phase_bits = generic_task<F32, CROP, HWC>(ga, t1, ring, bars, phase_bits);
     }
   }
 

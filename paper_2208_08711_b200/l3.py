@@ -51,6 +51,7 @@ class l3_decode_args(ctypes.Structure):
 
 
 L3_DECODE_HINT_WIDE = 1
+L3_DECODE_LAYOUT_HWC = 2
 
 
 class l3_encode_args(ctypes.Structure):

@@ -22,7 +22,8 @@ from paper_2208_08711_b200.api import IMAGENET_MEAN, IMAGENET_STD  # noqa: E402
 F32_TOL = 1e-6
 
 
-def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), canary=True, gap=0, wide=False):
+def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), canary=True, gap=0, wide=False,
+               layout="chw"):
     """Decode files on the GPU into per-image blocks (optionally separated by `gap` canary
     elements). Returns (list of arrays [3,H,W], status, bad_unit, flat output)."""
     src, offs = pack_files(files)
@@ -37,7 +38,7 @@ def gpu_decode(files, shapes, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0)
     dec = BatchDecoder(max(n, 1))
     sh = torch.tensor(np.array(shapes, np.int32).reshape(n, 2), device="cuda")
     st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(out_off).cuda(), scale=scale, bias=bias,
-                         wide=wide)
+                         wide=wide, layout=layout)
     torch.cuda.synchronize()
     flat = out.cpu().numpy()
     imgs = [flat[int(o):int(o) + s].reshape(3, h, w) for o, s, (h, w) in zip(out_off, sizes, shapes)]
@@ -206,11 +207,12 @@ def test_fault_injection_status_parity(seed):
     P = (-(-W // N)) * (-(-H // N))
     files = _corrupt_variants(rng, f, P) + [f]
     shapes = [(H, W)] * len(files)
-    for dtype, wide in ((torch.uint8, False), (torch.uint8, True), (torch.float32, False)):
-        _, st, bad, _, _, _ = gpu_decode(files, shapes, dtype=dtype, wide=wide)
+    for dtype, wide, layout in ((torch.uint8, False, "chw"), (torch.uint8, True, "chw"), (torch.float32, False, "chw"),
+                                (torch.uint8, False, "hwc"), (torch.float32, False, "hwc")):
+        _, st, bad, _, _, _ = gpu_decode(files, shapes, dtype=dtype, wide=wide, layout=layout)
         for i, fi in enumerate(files):
             rst, rbad, _, _ = l3ref.decode(fi, exp_shape=(H, W))
-            assert (st[i], bad[i]) == (rst, rbad), (dtype, wide, i, st[i], bad[i], rst, rbad)
+            assert (st[i], bad[i]) == (rst, rbad), (dtype, wide, layout, i, st[i], bad[i], rst, rbad)
 
 
 def test_shape_mismatch_is_corrupt_header():
@@ -289,7 +291,9 @@ def test_pipelined_loader_matches_direct_decode():
 
 # ------------------------------------------------------------------ f3: partial decode (crop / flip)
 
-def _crop_decode(files, shapes, crops, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0)):
+def _crop_decode(files, shapes, crops, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), layout="chw",
+                 use_crops=True):
+    """Decode into per-image window blocks; returns planar [3, h, w] arrays whatever the layout."""
     src, offs = pack_files(files)
     n = len(files)
     sizes = [3 * int(c[2]) * int(c[3]) for c in crops]
@@ -299,13 +303,17 @@ def _crop_decode(files, shapes, crops, dtype=torch.uint8, scale=(1, 1, 1), bias=
     out = torch.full((sum(sizes),), fill, dtype=dtype, device="cuda")
     dec = BatchDecoder(n)
     sh = torch.tensor(np.array(shapes, np.int32).reshape(n, 2), device="cuda")
-    cr = torch.tensor(np.array(crops, np.int32).reshape(n, 5), device="cuda")
+    cr = torch.tensor(np.array(crops, np.int32).reshape(n, 5), device="cuda") if use_crops else None
     st, bad = dec.decode(src, offs, sh, out, out_offsets=torch.from_numpy(oo).cuda(), scale=scale, bias=bias,
-                         crops=cr)
+                         crops=cr, layout=layout)
     torch.cuda.synchronize()
     flat = out.cpu().numpy()
-    return [flat[int(o):int(o) + s].reshape(3, int(c[2]), int(c[3])) for o, s, c in zip(oo, sizes, crops)], \
-        st.cpu().numpy()
+    if layout == "hwc":
+        blocks = [flat[int(o):int(o) + s].reshape(int(c[2]), int(c[3]), 3).transpose(2, 0, 1)
+                  for o, s, c in zip(oo, sizes, crops)]
+    else:
+        blocks = [flat[int(o):int(o) + s].reshape(3, int(c[2]), int(c[3])) for o, s, c in zip(oo, sizes, crops)]
+    return blocks, st.cpu().numpy()
 
 
 def _window(img, c):
@@ -338,6 +346,54 @@ def test_crop_flip_matches_oracle(seed):
             else:
                 assert np.abs(g.astype(np.float64) - l3ref.normalize(np.ascontiguousarray(ref), IMAGENET_MEAN,
                                                                      IMAGENET_STD)).max() <= F32_TOL
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("with_crop", [False, True])
+def test_hwc_layout_matches_oracle(seed, with_crop):
+    """f3: interleaved [h, w, 3] output (L3_DECODE_LAYOUT_HWC), full image or crop + flip, u8 and fp32."""
+    rng = np.random.default_rng(70 + seed)
+    imgs, files, crops = [], [], []
+    for i in range(9):
+        H, W = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        N = int(rng.choice([0, 7, 32, 64, 128, 200]))
+        im = l3synth.uniform_image(H, W, 90 * seed + i) if i % 2 else l3synth.natural(H, W, 90 * seed + i, 1.0)
+        imgs.append(im)
+        files.append(l3ref.encode(im, N=N))
+        if with_crop:
+            h = int(rng.integers(1, H + 1)); w = int(rng.integers(1, W + 1))
+            crops.append((int(rng.integers(0, H - h + 1)), int(rng.integers(0, W - w + 1)), h, w,
+                          int(rng.integers(0, 2))))
+        else:
+            crops.append((0, 0, H, W, 0))
+    for dtype in (torch.uint8, torch.float32):
+        scale, bias = ((1, 1, 1), (0, 0, 0)) if dtype == torch.uint8 else normalize_constants(IMAGENET_MEAN,
+                                                                                              IMAGENET_STD)
+        got, st = _crop_decode(files, [im.shape[1:] for im in imgs], crops, dtype, scale, bias, layout="hwc",
+                               use_crops=with_crop)
+        assert st.tolist() == [0] * len(files)
+        for g, im, c in zip(got, imgs, crops):
+            ref = _window(im, c)
+            if dtype == torch.uint8:
+                assert np.array_equal(g, ref), c
+            else:
+                assert np.abs(g.astype(np.float64) - l3ref.normalize(np.ascontiguousarray(ref), IMAGENET_MEAN,
+                                                                     IMAGENET_STD)).max() <= F32_TOL
+
+
+def test_hwc_config3_dense():
+    """Dense [n, H, W, 3] u8 output of Cityscapes-shaped images (out_offsets NULL)."""
+    imgs = l3synth.make_batch("c3_cityscapes", 3)
+    src, offs = pack_files([l3ref.encode(im) for im in imgs])
+    out = torch.full((3, 1024, 2048, 3), 0xA5, dtype=torch.uint8, device="cuda")
+    dec = BatchDecoder(3)
+    sh = torch.tensor([[1024, 2048]] * 3, dtype=torch.int32, device="cuda")
+    st, _ = dec.decode(src, offs, sh, out, layout="hwc")
+    torch.cuda.synchronize()
+    assert st.tolist() == [0, 0, 0]
+    got = out.cpu().numpy()
+    for i, im in enumerate(imgs):
+        assert np.array_equal(got[i], im.transpose(1, 2, 0))
 
 
 def test_crop_config3_random_crops():
