@@ -181,7 +181,9 @@ struct LaneRows {
   bool flip;          // horizontal flip of the window
 };
 
-template <bool F32, bool FAST>
+// FAST: aligned vector store. Otherwise scalar stores; RAGGED: the patch width is not a multiple of
+// 4, so the lane's trailing columns may lie outside it (else all 4 are stored unconditionally).
+template <bool F32, bool FAST, bool RAGGED = !FAST>
 __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi, bool pred) {
   if (F32) {
     const float v0 = fmaf((float)(xA & 0xFFFFu), sc, bi), v1 = fmaf((float)(xA >> 16), sc, bi);
@@ -194,9 +196,9 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
     } else if (pred) {
       float* o = reinterpret_cast<float*>(s.optr);
       o[0] = v0;
-      if (s.j4 + 1 < s.w) o[1] = v1;
-      if (s.j4 + 2 < s.w) o[2] = v2;
-      if (s.j4 + 3 < s.w) o[3] = v3;
+      if (!RAGGED || s.j4 + 1 < s.w) o[1] = v1;
+      if (!RAGGED || s.j4 + 2 < s.w) o[2] = v2;
+      if (!RAGGED || s.j4 + 3 < s.w) o[3] = v3;
     }
   } else {
     const uint32_t q = prmt(xA, xB, 0x6420);   // [c0, c1, c2, c3]
@@ -207,9 +209,9 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
     } else if (pred) {
       uint8_t* o = s.optr;
       o[0] = (uint8_t)q;
-      if (s.j4 + 1 < s.w) o[1] = (uint8_t)(q >> 8);
-      if (s.j4 + 2 < s.w) o[2] = (uint8_t)(q >> 16);
-      if (s.j4 + 3 < s.w) o[3] = (uint8_t)(q >> 24);
+      if (!RAGGED || s.j4 + 1 < s.w) o[1] = (uint8_t)(q >> 8);
+      if (!RAGGED || s.j4 + 2 < s.w) o[2] = (uint8_t)(q >> 16);
+      if (!RAGGED || s.j4 + 3 < s.w) o[3] = (uint8_t)(q >> 24);
     }
   }
 }
@@ -242,7 +244,7 @@ __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
 // STORE = false (HWC kernel): the row's pixels are left in s.A / s.B for an interleaving store.
 template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP, bool STORE = true, int SLOTS = kSlots,
-          bool HWC = false>
+          bool HWC = false, bool RAGGED = !FAST>
 __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
   const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
@@ -279,7 +281,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
     xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
   }
-  if (!FAST) {   // ragged patch: columns >= w are ghosts of column w-1
+  if (RAGGED) {   // ragged patch: columns >= w are ghosts of column w-1
     if (s.j4 + 1 >= s.w) xA = (xA & 0xFFu) * 0x00010001u;
     if (s.j4 + 2 >= s.w) xB = (xA >> 16) * 0x00010001u;
     if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
@@ -289,7 +291,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   } else if (CROP) {
     store4_crop<F32, HWC>(s, xA, xB, sc, bi, live && s.valid);
   } else {
-    store4<F32, FAST>(s, xA, xB, sc, bi, live && s.valid);
+    store4<F32, FAST, RAGGED>(s, xA, xB, sc, bi, live && s.valid);
   }
   s.A = xA;
   s.B = xB;
@@ -306,7 +308,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   }
 }
 
-template <bool F32, bool FAST, bool STREAM, bool CROP, bool HWC>
+template <bool F32, bool FAST, bool STREAM, bool CROP, bool HWC, bool RAGGED = !FAST>
 __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uint32_t hmax, uint32_t Lw, float sc,
                                                  float bi, uint32_t K, const uint8_t* src, uint64_t lim,
                                                  StreamState& st, uint64_t* bars, uint32_t& phase_bits,
@@ -315,18 +317,18 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
     stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
   s.raw = rbits(ring, s.bp);
-  decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, 0, Lw, sc, bi, K);
+  decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r, Lw, sc, bi, K);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r + 1, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r, Lw, sc, bi, K);
   }
 }
 
@@ -540,6 +542,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
                                                                    (F32 ? 15 : 3)) == 0) &&
                                                                  ((s.pitch & (F32 ? 15u : 3u)) == 0))));
     const bool fast = __all_sync(0xffffffffu, fast_ok);
+    // u8 narrow variant (small, mixed-shape images, e.g. C2): planar output that is not
+    // vector-aligned (image width not a multiple of 4) but has no ragged patch takes scalar stores
+    // without per-column tests or edge ghosts. Other variants keep two paths (code size, registers).
+    constexpr bool kAlignedOnlyPath = !F32 && !WIDE && !CROP;
+    const bool aligned_only = kAlignedOnlyPath && !fast && __all_sync(0xffffffffu, !active || (w & 3u) == 0);
     const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
     const float bi = F32 ? (ch == 0 ? p.bias[0] : (ch == 1 ? p.bias[1] : p.bias[2])) : 0.f;
     const uint32_t rowmax = (12u + 8u * 128u) / 8u + 10u;
@@ -547,11 +554,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
       if (stream) {
         if (fast)
           decode_unit_rows<F32, true, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+        else if constexpr (kAlignedOnlyPath) {
+          if (aligned_only)
+            decode_unit_rows<F32, false, true, CROP, HWC, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          else
+            decode_unit_rows<F32, false, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+        }
         else
           decode_unit_rows<F32, false, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       } else {
         if (fast)
           decode_unit_rows<F32, true, false, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+        else if constexpr (kAlignedOnlyPath) {
+          if (aligned_only)
+            decode_unit_rows<F32, false, false, CROP, HWC, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+          else
+            decode_unit_rows<F32, false, false, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
+        }
         else
           decode_unit_rows<F32, false, false, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       }
