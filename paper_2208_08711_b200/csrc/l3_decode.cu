@@ -152,7 +152,11 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
           d.G = 1;
         }
         d.tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
-        if (HWCK && d.mode != 3) {
+        if (HWCK && d.mode == 0) {   // N <= 32: G = 32 / L tiles (L-lane segments) per task
+          d.mode = 6;
+          d.G = 32u / d.L;
+          d.tasks = (d.P + d.G - 1) / d.G;
+        } else if (HWCK && d.mode != 3) {   // one tile per task, streamed
           d.mode = 5;
           d.tasks = d.P;
         }

@@ -542,9 +542,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
                                                                    (F32 ? 15 : 3)) == 0) &&
                                                                  ((s.pitch & (F32 ? 15u : 3u)) == 0))));
     const bool fast = __all_sync(0xffffffffu, fast_ok);
-    // u8 narrow variant (small, mixed-shape images, e.g. C2): planar output that is not
-    // vector-aligned (image width not a multiple of 4) but has no ragged patch takes scalar stores
-    // without per-column tests or edge ghosts. Other variants keep two paths (code size, registers).
+    // u8 narrow variant, whole-staged N <= 32 tasks (small mixed-shape images, e.g. C2): planar
+    // output that is not vector-aligned (image width not a multiple of 4) but has no ragged patch
+    // takes scalar stores without per-column tests or edge ghosts. Everything else keeps two paths
+    // (code size, registers: a third instantiation on the streamed path cost C3 5 %).
     constexpr bool kAlignedOnlyPath = !F32 && !WIDE && !CROP;
     const bool aligned_only = kAlignedOnlyPath && !fast && __all_sync(0xffffffffu, !active || (w & 3u) == 0);
     const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
@@ -554,12 +555,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
       if (stream) {
         if (fast)
           decode_unit_rows<F32, true, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
-        else if constexpr (kAlignedOnlyPath) {
-          if (aligned_only)
-            decode_unit_rows<F32, false, true, CROP, HWC, false>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
-          else
-            decode_unit_rows<F32, false, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
-        }
         else
           decode_unit_rows<F32, false, true, CROP, HWC>(s, ring, hmax, Lw, sc, bi, K, p.pp.src, lim, st, bars, phase_bits, rowmax, lane);
       } else {

@@ -27,9 +27,15 @@ __host__ __device__ constexpr size_t hwc_smem_bytes() {
   return (size_t)kHwcWarps * 3 * kHwcPitch + (size_t)kHwcWarps * 3 * kHwcSlots * 8 + 16;
 }
 
+// Store modes of the interleaved epilogue.
+constexpr int kStAligned = 0;   // every row start aligned (u8: 4 B, fp32: 16 B): 3 vector stores
+constexpr int kStDynamic = 1;   // rows of varying alignment (image width not a multiple of 4)
+constexpr int kStRagged = 2;    // the patch width is not a multiple of 4: per-column tests
+
 // Row r of a tile, 4 columns of this lane, interleaved: R0 G0 B0 R1 G1 B1 R2 G2 B2 R3 G3 B3.
-// r/g/b hold the row in pair form (A = columns 0, 1; B = columns 2, 3).
-template <bool F32, bool FAST>
+// r/g/b hold the row in pair form (A = columns 0, 1; B = columns 2, 3). kStDynamic picks the widest
+// store the row's alignment allows; it is uniform across the warp (lanes differ by 12 or 48 bytes).
+template <bool F32, int MODE>
 __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const LaneRows& g, const LaneRows& b,
                                         const float* sc, const float* bi, bool pred) {
   if (F32) {
@@ -42,7 +48,7 @@ __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const 
         const uint32_t pr = x[c][t >> 1];
         v[3 * t + c] = fmaf((float)((t & 1) ? (pr >> 16) : (pr & 0xFFFFu)), sc[c], bi[c]);
       }
-    if (FAST) {
+    if (MODE == kStAligned) {
 #pragma unroll
       for (int q = 0; q < 3; q++)
         asm volatile(
@@ -51,13 +57,25 @@ __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const 
             "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3]), "r"((uint32_t)pred));
     } else if (pred) {
       float* o = reinterpret_cast<float*>(optr);
+      if (MODE == kStRagged) {
 #pragma unroll
-      for (int t = 0; t < 4; t++)
-        if (r.j4 + t < r.w) {
-          o[3 * t] = v[3 * t];
-          o[3 * t + 1] = v[3 * t + 1];
-          o[3 * t + 2] = v[3 * t + 2];
-        }
+        for (int t = 0; t < 4; t++)
+          if (r.j4 + t < r.w) {
+            o[3 * t] = v[3 * t];
+            o[3 * t + 1] = v[3 * t + 1];
+            o[3 * t + 2] = v[3 * t + 2];
+          }
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 15u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+          reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 7u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; q++) reinterpret_cast<float2*>(o)[q] = make_float2(v[2 * q], v[2 * q + 1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 12; e++) o[e] = v[e];
+      }
     }
   } else {
     const uint32_t x = prmt(r.A, g.A, 0x6240);   // R0 G0 R1 G1
@@ -66,7 +84,7 @@ __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const 
     const uint32_t w0 = prmt(x, z, 0x2410);      // R0 G0 B0 R1
     const uint32_t w1 = prmt(prmt(x, z, 0x0053), y, 0x5410);   // G1 B1 R2 G2
     const uint32_t w2 = prmt(y, z, 0x7326);      // B2 R3 G3 B3
-    if (FAST) {
+    if (MODE == kStAligned) {
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
           "@p st.global.b32 [%0], %1;\n\t@p st.global.b32 [%0+4], %2;\n\t@p st.global.b32 [%0+8], %3;\n\t}" ::"l"(
@@ -74,47 +92,213 @@ __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const 
           "r"(w0), "r"(w1), "r"(w2), "r"((uint32_t)pred));
     } else if (pred) {
       const uint32_t wv[3] = {w0, w1, w2};
+      if (MODE == kStRagged) {
 #pragma unroll
-      for (int e = 0; e < 12; e++)
-        if (r.j4 + e / 3 < r.w) optr[e] = (uint8_t)(wv[e >> 2] >> (8 * (e & 3)));
+        for (int e = 0; e < 12; e++)
+          if (r.j4 + e / 3 < r.w) optr[e] = (uint8_t)(wv[e >> 2] >> (8 * (e & 3)));
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 3u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) reinterpret_cast<uint32_t*>(optr)[q] = wv[q];
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 1u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; q++)
+          reinterpret_cast<uint16_t*>(optr)[q] = (uint16_t)(wv[q >> 1] >> (16 * (q & 1)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 12; e++) optr[e] = (uint8_t)(wv[e >> 2] >> (8 * (e & 3)));
+      }
     }
   }
 }
 
-// The rows of one tile: per row, the three channels' ring tests, decode_row x 3, one store.
-template <bool F32, bool FAST>
+// The rows of one tile: per row, the three channels' ring tests (STREAM), decode_row x 3, one
+// interleaved store. Whole-staged tasks (!STREAM, N <= 32) run L-lane segments (GUARD).
+template <bool F32, int MODE, bool STREAM>
 __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint64_t* bars, StreamState* st,
                                               uint32_t* ph, uint32_t h, uint8_t* optr, uint32_t pitch,
                                               const float* sc, const float* bi, uint32_t K, const uint8_t* src,
-                                              uint64_t lim, int lane) {
+                                              uint64_t lim, int lane, uint32_t Lw, bool valid) {
+  constexpr bool FAST = MODE != kStRagged;   // no ghost columns
+  constexpr bool GUARD = !STREAM;
+  constexpr int SLOTS = STREAM ? kHwcSlots : 16;   // whole-staged: one linear 12 KB buffer, no wrap
   constexpr uint32_t rowmax = (12u + 8u * 128u) / 8u + 10u;
 #pragma unroll
   for (int c = 0; c < 3; c++) {
-    uint8_t* ring = rings + c * kHwcPitch;
-    if ((s[c].bp >> 3) + 2u * rowmax > st[c].landed_end)
+    uint8_t* ring = STREAM ? rings + c * kHwcPitch : rings;
+    if (STREAM && (s[c].bp >> 3) + 2u * rowmax > st[c].landed_end)
       stream_advance<kHwcSlots>(src, lim, st[c], ring, bars + c * kHwcSlots, ph[c], s[c].bp >> 3,
                                 (s[c].bp >> 3) + 2u * rowmax, lane);
-    s[c].raw = rbits<kHwcSlots>(ring, s[c].bp);
+    s[c].raw = rbits<SLOTS>(ring, s[c].bp);
   }
 #pragma unroll
   for (int c = 0; c < 3; c++)
-    decode_row<true, false, FAST, false, false, false, kHwcSlots>(s[c], rings + c * kHwcPitch, 0, 32u, 0.f, 0.f, K);
-  store12<F32, FAST>(optr, s[0], s[1], s[2], sc, bi, s[0].valid);
+    decode_row<true, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, 0, Lw,
+                                                              0.f, 0.f, K);
+  store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && s[0].h > 0);
   optr += pitch;
   for (uint32_t r = 1; r < h; r++) {
+    if (STREAM) {
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-      if ((s[c].bp >> 3) + rowmax > st[c].landed_end)
-        stream_advance<kHwcSlots>(src, lim, st[c], rings + c * kHwcPitch, bars + c * kHwcSlots, ph[c],
-                                  s[c].bp >> 3, (s[c].bp >> 3) + 2u * rowmax, lane);
+      for (int c = 0; c < 3; c++) {
+        if ((s[c].bp >> 3) + rowmax > st[c].landed_end)
+          stream_advance<kHwcSlots>(src, lim, st[c], rings + c * kHwcPitch, bars + c * kHwcSlots, ph[c],
+                                    s[c].bp >> 3, (s[c].bp >> 3) + 2u * rowmax, lane);
+      }
     }
 #pragma unroll
     for (int c = 0; c < 3; c++)
-      decode_row<false, false, FAST, false, false, false, kHwcSlots>(s[c], rings + c * kHwcPitch, r, 32u, 0.f, 0.f,
-                                                                     K);
-    store12<F32, FAST>(optr, s[0], s[1], s[2], sc, bi, s[0].valid);
+      decode_row<false, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, r,
+                                                                 Lw, 0.f, 0.f, K);
+    store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && r < s[0].h);
     optr += pitch;
   }
+}
+
+// N <= 32 (mode 6): G = 32 / L tiles per task, one L-lane segment each (as mode 0 of the planar
+// kernel). The task's 3G units are staged whole into the warp's 12 KB buffer with one barrier;
+// if they do not fit (near-incompressible content), the tiles are staged and decoded one per pass.
+template <bool F32>
+__device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const ImgDesc& d, int img, uint32_t t,
+                                                   uint8_t* buf, uint64_t* bars, uint32_t ph0, uint64_t lim,
+                                                   uint32_t K, int lane) {
+  constexpr uint32_t kCap = 3u * kHwcPitch - 64u;   // staging capacity (keeps the 8-byte reads in bounds)
+  const uint32_t esz = F32 ? 4u : 1u;
+  const uint32_t L = d.L, G = d.G;
+  const uint32_t seg = (uint32_t)lane / L, j = (uint32_t)lane % L;
+  const uint32_t tile = t * G + seg;
+  const bool tact = tile < d.P;
+  uint32_t x0 = 0, y0 = 0, w = 0, h = 0;
+  if (tact) {
+    x0 = (tile % d.gx) * d.N;
+    y0 = (tile / d.gx) * d.N;
+    w = min(d.N, d.W - x0);
+    h = min(d.N, d.H - y0);
+  }
+  const uint32_t nunits = 3u * d.P;
+  const uint8_t* file = p.pp.src + d.file_off;
+  const uint32_t worst = worst_patch_bytes(w, h);
+  uint64_t start[3], end[3], a16[3], sEnd[3];
+  uint32_t bytes[3], len[3];
+  bool act[3];
+  uint32_t total = 0;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const uint32_t u = (uint32_t)c * d.P + tile;
+    uint64_t off = 0, nxt = 0;
+    if (tact) {
+      off = ld_u32le(file + 13 + 4ull * u);
+      nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
+    }
+    act[c] = tact && !((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off));
+    if (tact && !act[c] && j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+    start[c] = act[c] ? d.data_off + off : 0;
+    end[c] = act[c] ? d.data_off + nxt : 0;
+    sEnd[c] = act[c] ? min(end[c], start[c] + worst + 8) : 0;
+    a16[c] = start[c] & ~15ull;
+    bytes[c] = act[c] ? (uint32_t)(((sEnd[c] + 15) & ~15ull) - a16[c]) : 0u;
+    len[c] = act[c] ? (uint32_t)min((uint64_t)(worst + 16), end[c] - start[c]) : 0u;
+    total += bytes[c];
+  }
+  // one pass if the task's units fit the buffer, else one tile per pass
+  uint32_t incl = (j == 0) ? total : 0u;   // inclusive scan over the segments (leader lanes)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t sum = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t seg_excl = __shfl_sync(0xffffffffu, incl, seg * L) - __shfl_sync(0xffffffffu, (j == 0) ? total : 0u,
+                                                                                   seg * L);
+  const bool one = sum <= kCap;
+  const uint32_t npass = one ? 1u : G;
+  const float sc[3] = {F32 ? p.scale[0] : 0.f, F32 ? p.scale[1] : 0.f, F32 ? p.scale[2] : 0.f};
+  const float bi[3] = {F32 ? p.bias[0] : 0.f, F32 ? p.bias[1] : 0.f, F32 ? p.bias[2] : 0.f};
+  const uint32_t pitch = d.W * 3u * esz;
+  for (uint32_t q = 0; q < npass; q++) {
+    const bool mine = tact && (one || seg == q);
+    const uint32_t base = one ? seg_excl : 0u;
+    // a2: stage this pass's units (bulk copies on bars[0], < 16 tail bytes past `lim` by the lanes)
+    uint32_t bulk[3], off_c[3];
+    uint32_t tx = 0, cum = 0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      off_c[c] = base + cum;
+      cum += bytes[c];
+      const uint64_t b16 = a16[c] + bytes[c];
+      const uint64_t be = b16 < lim ? b16 : lim;
+      bulk[c] = (mine && be > a16[c]) ? (uint32_t)(be - a16[c]) : 0u;
+      tx += bulk[c];
+    }
+    uint32_t txw = (mine && j == 0) ? tx : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) txw += __shfl_xor_sync(0xffffffffu, txw, o);
+    if (lane == 0) mbar_arrive_expect_tx(&bars[0], txw);
+    __syncwarp();
+    if (mine) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        uint8_t* dst = buf + off_c[c];
+        if (j == 0 && bulk[c]) bulk_g2s(dst, p.pp.src + a16[c], bulk[c], &bars[0]);
+        const uint64_t b16 = a16[c] + bytes[c];
+        const uint64_t t0 = a16[c] > lim ? a16[c] : lim;
+        for (uint64_t x = t0 + j; x < sEnd[c] && x < b16; x += L) dst[x - a16[c]] = __ldg(p.pp.src + x);
+      }
+    }
+    mbar_wait(&bars[0], ph0 & 1u);
+    ph0 ^= 1u;
+    __syncwarp();
+    if (mine) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) swap_words(buf + off_c[c], 0, bytes[c], j, L);
+    }
+    __syncwarp();
+    // a3-a6
+    LaneRows s[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      s[c].w = w;
+      s[c].h = (mine && act[c]) ? h : 0u;
+      s[c].j4 = 4u * j;
+      s[c].first = (j == 0);
+      s[c].last = (s[c].j4 + 4u >= w);
+      s[c].valid = mine && s[c].j4 < w;
+      s[c].kacc = 0;
+      s[c].A = s[c].B = 0;
+      s[c].bp = (off_c[c] + (uint32_t)(start[c] - a16[c])) * 8u;
+      s[c].lim = s[c].bp + len[c] * 8u;
+    }
+    uint32_t hmax = mine ? h : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    uint8_t* optr = reinterpret_cast<uint8_t*>(p.out) + (d.out_off + ((uint64_t)y0 * d.W + x0 + 4u * j) * 3u) * esz;
+    const bool ragged = __any_sync(0xffffffffu, mine && (w & 3u) != 0);
+    const bool aligned = __all_sync(0xffffffffu, !mine || ((reinterpret_cast<uintptr_t>(optr) & (F32 ? 15 : 3)) == 0 &&
+                                                          (pitch & (F32 ? 15u : 3u)) == 0));
+    const bool valid = s[0].valid && s[1].h > 0 && s[2].h > 0;
+    StreamState* nost = nullptr;
+    if (hmax > 0) {
+      if (ragged)
+        hwc_tile_rows<F32, kStRagged, false>(s, buf, bars, nost, nullptr, hmax, optr, pitch, sc, bi, K, p.pp.src,
+                                             lim, lane, L, valid);
+      else if (aligned)
+        hwc_tile_rows<F32, kStAligned, false>(s, buf, bars, nost, nullptr, hmax, optr, pitch, sc, bi, K, p.pp.src,
+                                              lim, lane, L, valid);
+      else
+        hwc_tile_rows<F32, kStDynamic, false>(s, buf, bars, nost, nullptr, hmax, optr, pitch, sc, bi, K, p.pp.src,
+                                              lim, lane, L, valid);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const bool err = mine && act[c] && (s[c].kacc >= 0x80000000u || s[c].bp > s[c].lim);
+      if (err && j == 0) {   // a7: exact first error of a failed unit
+        const int code = unit_first_error(p.pp.src, start[c], end[c], w, h);
+        if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
+      }
+    }
+    __syncwarp();
+    fence_proxy_async_smem();
+  }
+  return ph0;
 }
 
 template <bool F32>
@@ -163,9 +347,14 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     }
     const int img = lo;
     const ImgDesc d = p.pp.ws.desc[img];
-    const uint32_t pp = (uint32_t)(task - prefix[img]);   // patch index: the tile
+    const uint32_t pp = (uint32_t)(task - prefix[img]);   // patch index: the tile (mode 6: tile group)
     uint64_t next = 0;
     if (lane == 0) next = atomicAdd(&head->next_task[0], 1ull);
+    if (d.mode == 6) {   // N <= 32: G tiles per task, whole-staged
+      ph[0] = hwc_small_task<F32>(p, d, img, pp, rings, bars, ph[0], lim, K, lane);
+      task = __shfl_sync(0xffffffffu, next, 0);
+      continue;
+    }
 
     const uint32_t px = pp % d.gx, py = pp / d.gx;
     const uint32_t x0 = px * d.N, y0 = py * d.N;
@@ -216,15 +405,21 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     const uint32_t pitch = d.W * 3u * esz;
     uint8_t* optr = reinterpret_cast<uint8_t*>(p.out) +
                     (d.out_off + ((uint64_t)y0 * d.W + x0 + 4u * lane) * 3u) * esz;
-    const bool fast_ok = (w & 3u) == 0 && (reinterpret_cast<uintptr_t>(optr) & (F32 ? 15 : 3)) == 0 &&
-                         (pitch & (F32 ? 15u : 3u)) == 0;
-    const bool fast = __all_sync(0xffffffffu, fast_ok);
+    const bool aligned = (reinterpret_cast<uintptr_t>(optr) & (F32 ? 15 : 3)) == 0 && (pitch & (F32 ? 15u : 3u)) == 0;
+    const bool ragged = (w & 3u) != 0;   // warp-uniform: one tile per warp
+    const bool aligned_all = __all_sync(0xffffffffu, aligned);
     const float sc[3] = {F32 ? p.scale[0] : 0.f, F32 ? p.scale[1] : 0.f, F32 ? p.scale[2] : 0.f};
     const float bi[3] = {F32 ? p.bias[0] : 0.f, F32 ? p.bias[1] : 0.f, F32 ? p.bias[2] : 0.f};
-    if (fast)
-      hwc_tile_rows<F32, true>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane);
+    const bool valid = s[0].valid;
+    if (ragged)
+      hwc_tile_rows<F32, kStRagged, true>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane,
+                                          32u, valid);
+    else if (aligned_all)
+      hwc_tile_rows<F32, kStAligned, true>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane,
+                                           32u, valid);
     else
-      hwc_tile_rows<F32, false>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane);
+      hwc_tile_rows<F32, kStDynamic, true>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane,
+                                           32u, valid);
 
 #pragma unroll
     for (int c = 0; c < 3; c++) {
