@@ -90,17 +90,24 @@ if __name__ == "__main__":
     cases = {"c3_f32": ("c3_cityscapes_f32", 32 * 3 * 2048 * 1024, "C3 Cityscapes 32x2048x1024, fp32 out"),
              "c3_u8": ("c3_cityscapes_u8", 32 * 3 * 2048 * 1024, "C3 Cityscapes 32x2048x1024, u8 out"),
              "c4_u8": ("c4_uhd_u8", 16 * 3 * 3840 * 2160, "C4 UHD 16x3840x2160, u8 out (wide variant)"),
-             "c2_u8": ("c2_imagenet_u8", c2, "C2 ImageNet-shaped 256 x ~500x375, u8 out")}
+             "c2_u8": ("c2_imagenet_u8", c2, "C2 ImageNet-shaped 256 x ~500x375, u8 out"),
+             "c3_f32_hwc": ("c3_cityscapes_f32_hwc", 32 * 3 * 2048 * 1024,
+                            "C3 Cityscapes 32x2048x1024, fp32 HWC out (tile kernel, f3)")}
     for key, (tkey, samples, title) in cases.items():
         rep = f"{gp}_prof_{key}.ncu-rep"
         if not os.path.exists(rep):
             continue
         md, t = kernel_md(rep, samples)
+        lines = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_lines.py"), rep, "30"],
+                               capture_output=True, text=True).stdout
         traffic[tkey] = t
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{key}.md"), "w") as f:
             f.write(f"# {tag}: ncu --set full, decode kernel, {title}\n\n")
             f.write(f"Source: `{os.path.basename(rep)}` (one launch, `-s 3 -c 1`, --clock-control none).\n\n")
             f.write(md)
+            if lines:
+                f.write("\n## Hottest source lines (share of warp instructions, share of stall samples)\n\n```\n")
+                f.write(lines + "```\n")
     lc = f"{gp}_launches_c3_f32.csv"
     if os.path.exists(lc):
         with open(os.path.join(ROOT, "profiles", f"{tag}_launches_c3_f32.md"), "w") as f:
