@@ -172,6 +172,13 @@ l3_status_t l3_decode_batch_ablation(const l3_decode_args* args, int32_t mode, l
  */
 l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream);
 
+/* Exhaustive self-test of the byte-form 4-sample predictor used by the planar
+ * and crop decode paths (same rule, Fig. 3; ties TL, T, TR): for
+ * every triple and every sample position q in 0..3 of a lane's 4 columns.
+ * out: device, 4 * 2^24 bytes; out[q << 24 | TL<<16 | T<<8 | TR] = predicted byte.
+ * Returns INVALID_ARGUMENT for a NULL out, CUDA on a launch error; async. */
+l3_status_t l3_selftest_paeth4(uint8_t* out, l3_stream_t stream);
+
 /* Human-readable name of a status code; never NULL. */
 const char* l3_status_string(int32_t status);
 

@@ -532,6 +532,36 @@ cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Exhaustive self-test of the byte-form 4-sample predictor (paeth_pred4): for every
+// triple x = TL<<16 | T<<8 | TR and every sample position q in 0..3, a 6-byte row
+// c[-1..4] holds the triple at c[q-1], c[q], c[q+1] (other bytes: a hash of x, q),
+// and out[q << 24 | x] = the predicted byte of sample q.
+__global__ void l3_selftest_paeth4_kernel(uint8_t* out) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= (1u << 24)) return;
+#pragma unroll
+  for (uint32_t q = 0; q < 4; q++) {
+    uint32_t hsh = (x + 0x9E3779B9u * (q + 1u)) * 0x85EBCA6Bu;
+    hsh ^= hsh >> 13;
+    hsh *= 0xC2B2AE35u;
+    uint8_t c[6];   // c[i + 1] = column i, i = -1..4
+#pragma unroll
+    for (int i = 0; i < 6; i++) c[i] = (uint8_t)(hsh >> (4 * i));
+    c[q] = (uint8_t)(x >> 16);       // column q - 1: TL
+    c[q + 1] = (uint8_t)(x >> 8);    // column q: T
+    c[q + 2] = (uint8_t)x;           // column q + 1: TR
+    const uint32_t L = c[0] | (c[1] << 8) | (c[2] << 16) | ((uint32_t)c[3] << 24);
+    const uint32_t Q = c[1] | (c[2] << 8) | (c[3] << 16) | ((uint32_t)c[4] << 24);
+    const uint32_t R = c[2] | (c[3] << 8) | (c[4] << 16) | ((uint32_t)c[5] << 24);
+    out[(q << 24) | x] = (uint8_t)(paeth_pred4(L, Q, R) >> (8 * q));
+  }
+}
+
+cudaError_t launch_selftest_paeth4(uint8_t* out, cudaStream_t s) {
+  l3_selftest_paeth4_kernel<<<(1u << 24) / 256, 256, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
 // ============================================================== host launch
 static int g_sm_count = 0;
 // f32, u8 narrow, u8 wide, f32 crop, u8 crop, f32 wide, f32 HWC tile, u8 HWC tile, f32 crop HWC, u8 crop HWC

@@ -161,6 +161,42 @@ __device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_
   return prmt(X, tr, sel);                   // pair form: bytes 1 and 3 are zero
 }
 
+#ifndef L3_PRED4
+#define L3_PRED4 0   // 1: byte-form 4-sample predictor on the storing paths (A/B option; slower)
+#endif
+
+// Custom Paeth predictor (Fig. 3; ties TL, T, TR — reading C3)
+// for the lane's 4 samples in byte form. The candidates of sample i are
+// c[i-1], c[i], c[i+1] of the previous row; L = [c-1 c0 c1 c2], Q = [c0 c1 c2 c3],
+// R = [c1 c2 c3 c4] (edge-clamped by the caller's selectors). With u = |TL-T|,
+// v = |TR-T|, w = |TL-TR| the distances to ref = TL+TR-T are d(TL) = v, d(TR) = u and
+// d(T) = |TL+TR-2T|, which is |u-v| when T lies between TL and TR (then w = u+v) and
+// u+v >= max(u,v) when it does not (then w = |u-v|, and T can never be the
+// strict minimum, so its distance may be replaced by 255). So the per-sample
+// distances fit a byte: keys are dist << 8 | code in 16x2 halves (samples 0,2 in
+// pair A, 1,3 in pair B), one VIMNMX3.U16x2 per pair picks min distance, ties by
+// code order TL < T < TR, and the winning codes are directly the nibbles of a
+// PRMT selector into (L, R) bytes: sample i's candidates live at L/R byte indices
+// {0,1,2}, {1,2,3}, {2,3,6}, {3,6,7} for i = 0..3 (monotone in tie rank).
+// DESIGN.md §5 (byte-form predictor); exhaustively checked by l3_selftest_paeth4.
+__device__ __forceinline__ uint32_t paeth_pred4(uint32_t L, uint32_t Q, uint32_t R) {
+  const uint32_t U = __vabsdiffu4(L, Q);   // u_i = d(TR)
+  const uint32_t V = __vabsdiffu4(R, Q);   // v_i = d(TL)
+  const uint32_t W = __vabsdiffu4(L, R);   // w_i
+  const uint32_t D = __vabsdiffu4(U, V);   // |u - v|
+  // bytes with W == D (T not strictly between TL and TR): force d(T) = 255
+  const uint32_t a = (W ^ D) & 0x7F7F7F7Fu;
+  const uint32_t b = a + 0x7F7F7F7Fu;       // bit 7 set iff the low 7 bits of W^D are non-zero
+  const uint32_t c = ~(b | (W ^ D));        // bit 7 of byte i set iff W_i == D_i
+  const uint32_t Dm = D | prmt(c, 0u, 0xBA98u);   // sign-replicate bit 7 of each byte
+  // keys: byte 1 / 3 of each half = distance, byte 0 / 2 = code (PRMT from the code words)
+  constexpr uint32_t kCodeTL = 0x30021000u, kCodeT = 0x60032001u, kCodeTR = 0x70063002u;
+  const uint32_t mA = __vimin3_u16x2(prmt(V, kCodeTL, 0x2604u), prmt(Dm, kCodeT, 0x2604u), prmt(U, kCodeTR, 0x2604u));
+  const uint32_t mB = __vimin3_u16x2(prmt(V, kCodeTL, 0x3715u), prmt(Dm, kCodeT, 0x3715u), prmt(U, kCodeTR, 0x3715u));
+  const uint32_t t = mA | mB;               // byte 0: code0 | code1 << 4, byte 2: code2 | code3 << 4
+  return prmt(L, R, prmt(t, 0u, 0x0020u));
+}
+
 // Row reconstruction state of one lane: 4 consecutive columns j4..j4+3.
 struct LaneRows {
   uint32_t bp;        // unwrapped ring bit position of the current row header
@@ -173,7 +209,11 @@ struct LaneRows {
   bool first, last, valid;
   uint8_t* optr;      // output of column j4 in the current row
   uint32_t pitch;     // bytes between output rows
-  uint32_t A, B;      // previous row, pair form: A = (c0, c1), B = (c2, c3)
+  uint32_t A, B;      // previous row, pair form: A = (c0, c1), B = (c2, c3) (pair-predictor paths)
+  uint32_t Q;         // previous row, byte form [c0 c1 c2 c3] (byte-predictor paths)
+  uint32_t selL;      // PRMT selector (left lane's Q, Q) -> [c-1 c0 c1 c2], clamped at column 0
+  uint32_t selR;      // PRMT selector (Q, right lane's Q) -> [c1 c2 c3 c4], clamped at the last lane
+  uint32_t selG;      // RAGGED: PRMT selector replicating column w-1 into the lane's ghost columns
   // CROP variant only (f3, partial decode): output window mapping
   int32_t ri;         // current image row - crop top
   int32_t cj0;        // first column of this lane - crop left
@@ -216,12 +256,47 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
   }
 }
 
+// Byte-form variant of store4: q = [c0 c1 c2 c3].
+template <bool F32, bool FAST, bool RAGGED = !FAST>
+__device__ __forceinline__ void store4q(const LaneRows& s, uint32_t q, float sc, float bi, bool pred) {
+  if (F32) {
+    const float v0 = fmaf((float)(q & 0xFFu), sc, bi), v1 = fmaf((float)((q >> 8) & 0xFFu), sc, bi);
+    const float v2 = fmaf((float)((q >> 16) & 0xFFu), sc, bi), v3 = fmaf((float)(q >> 24), sc, bi);
+    if (FAST) {   // predicated STG.128, no branch
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+          "@p st.global.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(s.optr),
+          "f"(v0), "f"(v1), "f"(v2), "f"(v3), "r"((uint32_t)pred));
+    } else if (pred) {
+      float* o = reinterpret_cast<float*>(s.optr);
+      o[0] = v0;
+      if (!RAGGED || s.j4 + 1 < s.w) o[1] = v1;
+      if (!RAGGED || s.j4 + 2 < s.w) o[2] = v2;
+      if (!RAGGED || s.j4 + 3 < s.w) o[3] = v3;
+    }
+  } else {
+    if (FAST) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+          "@p st.global.b32 [%0], %1;\n\t}" ::"l"(s.optr), "r"(q), "r"((uint32_t)pred));
+    } else if (pred) {
+      uint8_t* o = s.optr;
+      o[0] = (uint8_t)q;
+      if (!RAGGED || s.j4 + 1 < s.w) o[1] = (uint8_t)(q >> 8);
+      if (!RAGGED || s.j4 + 2 < s.w) o[2] = (uint8_t)(q >> 16);
+      if (!RAGGED || s.j4 + 3 < s.w) o[3] = (uint8_t)(q >> 24);
+    }
+  }
+}
+
 // f3: store the lane's 4 samples into a cropped (optionally flipped) window, planar or HWC.
-template <bool F32, bool HWC>
+template <bool F32, bool HWC, bool BYTES = false>
 __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi,
                                             bool pred) {
   if (!pred || (uint32_t)s.ri >= s.chh) return;
-  const uint32_t x[4] = {xA & 0xFFFFu, xA >> 16, xB & 0xFFFFu, xB >> 16};
+  // pair form (xA, xB), or (BYTES) byte form [c0 c1 c2 c3] in xA
+  const uint32_t x[4] = {BYTES ? (xA & 0xFFu) : (xA & 0xFFFFu), BYTES ? ((xA >> 8) & 0xFFu) : (xA >> 16),
+                         BYTES ? ((xA >> 16) & 0xFFu) : (xB & 0xFFFFu), BYTES ? (xA >> 24) : (xB >> 16)};
   const uint64_t row = (uint64_t)(uint32_t)s.ri * s.cw;
 #pragma unroll
   for (int t = 0; t < 4; t++) {
@@ -265,7 +340,28 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   const uint32_t d3 = shr_c(field * (pk * pk * pk), sh);
   const uint32_t dA = d1 * 0x10000u + d0 + base2;
   const uint32_t dB = d3 * 0x10000u + d2 + base2;
+  constexpr bool P4 = STORE && (L3_PRED4 != 0);   // byte-form predictor (planar / crop stores)
   uint32_t xA, xB;
+  if (P4) {
+    if (FIRST) {
+      xA = dA;
+      xB = dB;
+    } else {
+      // a5: row-wise parallel custom Paeth, 4 samples in byte form
+      const uint32_t Lq = __shfl_up_sync(0xffffffffu, s.Q, 1, Lw);     // left lane's [c-4 .. c-1]
+      const uint32_t Rq = __shfl_down_sync(0xffffffffu, s.Q, 1, Lw);   // right lane's [c4 .. c7]
+      const uint32_t L = prmt(Lq, s.Q, s.selL);   // [c-1 c0 c1 c2]; column 0: c-1 := c0 (reading C4)
+      const uint32_t R = prmt(s.Q, Rq, s.selR);   // [c1 c2 c3 c4]; last lane: c4 := c3 (C4; ghosts when ragged)
+      const uint32_t pr = paeth_pred4(L, s.Q, R);
+      xA = prmt(pr, 0u, 0x4140u) + dA;   // pair form (c0, c1) + residual; carries land in bytes 1, 3
+      xB = prmt(pr, 0u, 0x4342u) + dB;
+    }
+    uint32_t q = prmt(xA, xB, 0x6420u);   // [c0 c1 c2 c3] mod 256
+    if (RAGGED) q = prmt(q, 0u, s.selG);  // columns >= w: ghosts of column w-1
+    if (CROP) store4_crop<F32, HWC, true>(s, q, 0u, sc, bi, live && s.valid);
+    else store4q<F32, FAST, RAGGED>(s, q, sc, bi, live && s.valid);
+    s.Q = q;
+  } else {
   if (FIRST) {
     xA = dA & 0x00FF00FFu;
     xB = dB & 0x00FF00FFu;
@@ -295,6 +391,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   }
   s.A = xA;
   s.B = xB;
+  }
   if (live) {
     s.kacc = max(s.kacc, s.raw - 0x10000000u);
     s.bp = nbp;
@@ -471,6 +568,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     s.valid = active && (s.j4 < w);
     s.kacc = 0;
     s.A = s.B = 0;
+    s.Q = 0;
+    s.selL = s.first ? 0x6544u : 0x6543u;
+    s.selR = s.last ? 0x3321u : 0x4321u;
+    s.selG = (w >= s.j4 + 4u) ? 0x3210u : (w == s.j4 + 3u) ? 0x2210u : (w == s.j4 + 2u) ? 0x1110u : 0x0000u;
     const uint32_t esz = F32 ? 4u : 1u;
     if (CROP) {   // augment variant (f3): window, flip; planar, or HWC (interleaved channels)
       s.optr = reinterpret_cast<uint8_t*>(p.out) +
