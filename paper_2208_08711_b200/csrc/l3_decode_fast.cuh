@@ -161,6 +161,9 @@ __device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_
   return prmt(X, tr, sel);                   // pair form: bytes 1 and 3 are zero
 }
 
+#ifndef L3_EDGE_SEL
+#define L3_EDGE_SEL 0   // 1: patch-edge clamps by per-lane PRMT selectors instead of selects (A/B option)
+#endif
 #ifndef L3_PRED4
 #define L3_PRED4 0   // 1: byte-form 4-sample predictor on the storing paths (A/B option; slower)
 #endif
@@ -369,11 +372,18 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     // a5: row-wise parallel custom Paeth
     const uint32_t Bl = __shfl_up_sync(0xffffffffu, s.B, 1, Lw);     // left lane's (c2, c3)
     const uint32_t Ar = __shfl_down_sync(0xffffffffu, s.A, 1, Lw);   // right lane's (c0, c1)
+#if L3_EDGE_SEL
+    // edge clamps folded into per-lane PRMT selectors (no select per row)
+    const uint32_t TLA = prmt(Bl, s.A, s.selL);       // (c-1, c0); column 0: (c0, c0) (C4)
+    const uint32_t TRA = prmt(s.A, s.B, 0x5412);      // (c1, c2) = TL of pair B
+    const uint32_t TRB = prmt(s.B, Ar, s.selR);       // (c3, c+4); last lane: (c3, c3) (C4; ghosts when ragged)
+#else
     const uint32_t LF = s.first ? (s.A << 16) : Bl;   // byte 2 = TL of column j4 (C4: T at column 0)
     const uint32_t RT = s.last ? (s.B >> 16) : Ar;    // byte 0 = TR of column j4+3 (C4; ghosts when ragged)
     const uint32_t TLA = prmt(LF, s.A, 0x5452);       // (c-1, c0)
     const uint32_t TRA = prmt(s.A, s.B, 0x5412);      // (c1, c2) = TL of pair B
     const uint32_t TRB = prmt(s.B, RT, 0x5412);       // (c3, c+4)
+#endif
     xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
     xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
   }
@@ -569,8 +579,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : 0)
     s.kacc = 0;
     s.A = s.B = 0;
     s.Q = 0;
+#if L3_PRED4
     s.selL = s.first ? 0x6544u : 0x6543u;
     s.selR = s.last ? 0x3321u : 0x4321u;
+#else
+    s.selL = s.first ? 0x5454u : 0x5452u;   // L3_EDGE_SEL: TLA = prmt(left lane's B, A, selL)
+    s.selR = s.last ? 0x5212u : 0x5412u;    // L3_EDGE_SEL: TRB = prmt(B, right lane's A, selR)
+#endif
     s.selG = (w >= s.j4 + 4u) ? 0x3210u : (w == s.j4 + 3u) ? 0x2210u : (w == s.j4 + 2u) ? 0x1110u : 0x0000u;
     const uint32_t esz = F32 ? 4u : 1u;
     if (CROP) {   // augment variant (f3): window, flip; planar, or HWC (interleaved channels)
