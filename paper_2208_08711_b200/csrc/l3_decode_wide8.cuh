@@ -148,6 +148,25 @@ __device__ __forceinline__ void store8(const Lane8& s, uint32_t xA, uint32_t xB,
   }
 }
 
+#ifndef L3_PRED4_WIDE
+#define L3_PRED4_WIDE 0   // 1: byte-form predictor on the u8 wide path (A/B option)
+#endif
+
+// u8 store of the lane's 8 samples in byte form.
+template <bool FAST>
+__device__ __forceinline__ void store8q(const Lane8& s, uint32_t q0, uint32_t q1, bool pred) {
+  if (FAST) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+        "@p st.global.v2.b32 [%0], {%1, %2};\n\t}" ::"l"(s.optr), "r"(q0), "r"(q1), "r"((uint32_t)pred));
+  } else if (pred) {
+    uint8_t* o = s.optr;
+#pragma unroll
+    for (int c = 0; c < 8; c++)
+      if (s.j8 + c < s.w) o[c] = (uint8_t)((c < 4 ? q0 : q1) >> (8 * (c & 3)));
+  }
+}
+
 // One row of one lane (a3-a6) — see decode_row in l3_decode_fast.cuh for the
 // validity accumulation; this is the same step on 8 columns.
 template <bool FIRST, bool F32, bool FAST, bool GUARD, int SLOTS>
@@ -169,6 +188,48 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
   unpack4(f0, sh, pk, pk2, pk3, base2, dA, dB);
   unpack4(g1, sh, pk, pk2, pk3, base2, dC, dD);
   uint32_t xA, xB, xC, xD;
+  if constexpr (!F32 && L3_PRED4_WIDE != 0) {
+    // byte-form predictor (paeth_pred4), state s.A = [c0..c3], s.B = [c4..c7]
+    if (FIRST) {
+      xA = dA;
+      xB = dB;
+      xC = dC;
+      xD = dD;
+    } else {
+      const uint32_t Lq = __shfl_up_sync(0xffffffffu, s.B, 1, L);     // left lane's [c-4 .. c-1]
+      const uint32_t Rq = __shfl_down_sync(0xffffffffu, s.A, 1, L);   // right lane's [c8 .. c11]
+      const uint32_t L0 = prmt(Lq, s.A, 0x6543u + (uint32_t)s.first);           // [c-1 c0 c1 c2] (C4)
+      const uint32_t R0 = prmt(s.A, s.B, 0x4321u);                               // [c1 c2 c3 c4]
+      const uint32_t L1 = prmt(s.A, s.B, 0x6543u);                               // [c3 c4 c5 c6]
+      const uint32_t R1 = prmt(s.B, Rq, 0x4321u - ((uint32_t)s.last << 12));     // [c5 c6 c7 c8] (C4)
+      const uint32_t p0 = paeth_pred4(L0, s.A, R0), p1 = paeth_pred4(L1, s.B, R1);
+      xA = prmt(p0, 0u, 0x4140u) + dA;
+      xB = prmt(p0, 0u, 0x4342u) + dB;
+      xC = prmt(p1, 0u, 0x4140u) + dC;
+      xD = prmt(p1, 0u, 0x4342u) + dD;
+    }
+    uint32_t q0 = prmt(xA, xB, 0x6420u), q1 = prmt(xC, xD, 0x6420u);
+    if (!FAST) {   // ragged patch: columns >= w are ghosts of column w-1
+      uint32_t x[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) x[c] = ((c < 4 ? q0 : q1) >> (8 * (c & 3))) & 0xFFu;
+#pragma unroll
+      for (int c = 1; c < 8; c++)
+        if (s.j8 + c >= s.w) x[c] = x[c - 1];
+      q0 = x[0] | (x[1] << 8) | (x[2] << 16) | (x[3] << 24);
+      q1 = x[4] | (x[5] << 8) | (x[6] << 16) | (x[7] << 24);
+    }
+    store8q<FAST>(s, q0, q1, live && s.valid);
+    s.A = q0;
+    s.B = q1;
+    if (live) {
+      s.kacc = max(s.kacc, s.raw - 0x10000000u);
+      s.bp = nbp;
+      s.raw = raw_next;
+    }
+    s.optr += s.pitch;
+    return;
+  }
   if (FIRST) {
     xA = dA & 0x00FF00FFu;
     xB = dB & 0x00FF00FFu;
