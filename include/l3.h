@@ -90,7 +90,8 @@ typedef void* l3_stream_t;
 /* l3_decode_args.flags */
 #define L3_DECODE_HINT_WIDE 1u   /* u8 out: most files use 33 <= N <= 128 (e.g. policy N = 128 for
                                     >= FHD images): pick the 8-column-per-lane kernel variant.
-                                    A performance hint only; every file decodes correctly either way. */
+                                    A performance hint only; every file decodes correctly either way.
+                                    Ignored for L3_OUT_F32 and with crops. */
 #define L3_DECODE_LAYOUT_HWC 2u  /* f3: interleaved output, element (y, x, c) of image i
                                     at out_offsets[i] + (y * W + x) * 3 + c (W = window width with
                                     crops), u8 or f32 per out_kind; the channel planes of the file
@@ -111,7 +112,11 @@ typedef struct {
   void* workspace;
   uint64_t workspace_bytes;
   uint32_t flags;   /* L3_DECODE_HINT_* bits, 0 = none */
-  uint32_t reserved;
+  uint32_t max_ctas;      /* 0: the persistent decode grid covers every SM (SMs x resident CTAs);
+                             else at most max_ctas thread blocks, i.e. the decoder's share of the
+                             GPU is capped so that a concurrent (higher-priority) compute kernel
+                             keeps the remaining SMs ("We prioritize the computing
+                             stream over the decoding stream"). Any value decodes correctly. */
   const int32_t* crops;   /* device, n x {y, x, h, w, flip} or NULL (partial decode) */
 } l3_decode_args;
 

@@ -23,19 +23,20 @@ IMAGENET_STD = (0.229, 0.224, 0.225)
 
 
 def wide_hint(shapes_hw, out_dtype) -> bool:
-    """The L3_DECODE_HINT_WIDE choice for a batch (a performance hint only): u8 output, most images
-    large enough for the policy to pick N > 32 (>= 1080x720 pixels), and enough
-    patches (>= 16k units, e.g. 16 x UHD) that 2-patch tasks still keep every warp busy
-    (measured: wins on config 4, loses on 32 x 2048x1024)."""
+    """The L3_DECODE_HINT_WIDE choice for a batch (a performance hint only; u8 output): most images
+    get a patch size N > 32 from the encoder's policy (asked of the library through
+    l3_choose_patch_size) and the batch has enough patches (>= 16k units, e.g. 16 x UHD) that
+    2-patch tasks still keep every warp busy (measured: wins on config 4, loses on 32 x 2048x1024;
+    DESIGN.md §5)."""
     if out_dtype != torch.uint8 or len(shapes_hw) == 0:
         return False
     big = 0
     units = 0
     for h, w in shapes_hw:
         h, w = int(h), int(w)
-        n = 32 if h * w < 777600 else (64 if h * w < 2073600 else 128)
+        n = l3.l3_choose_patch_size(w, h)
         units += 3 * (-(-h // n)) * (-(-w // n))
-        big += h * w >= 1080 * 720
+        big += n > 32
     return 2 * big >= len(shapes_hw) and units >= 16384
 
 
@@ -60,7 +61,7 @@ class BatchDecoder:
         self.bad_unit = torch.empty(max_n, dtype=torch.int32, device=self.device)
 
     def args(self, src, src_offsets, shapes, out, *, out_offsets=None, scale=(1.0, 1.0, 1.0),
-             bias=(0.0, 0.0, 0.0), wide=False, crops=None, layout="chw"):
+             bias=(0.0, 0.0, 0.0), wide=False, crops=None, layout="chw", max_ctas=0):
         n = int(shapes.shape[0])
         if layout not in ("chw", "hwc"):
             raise ValueError(f"layout must be 'chw' or 'hwc', got {layout!r}")
@@ -69,17 +70,18 @@ class BatchDecoder:
             raise ValueError(f"batch of {n} > max_n={self.max_n}")
         return l3.make_decode_args(src, src_offsets, shapes, out, self.status[:n], self.workspace,
                                    out_offsets=out_offsets, bad_unit=self.bad_unit[:n], scale=scale, bias=bias,
-                                   flags=flags, crops=crops)
+                                   flags=flags, crops=crops, max_ctas=max_ctas)
 
     def decode(self, src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor,
                out: torch.Tensor, *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0),
-               stream=None, wide=False, crops=None, layout="chw"):
+               stream=None, wide=False, crops=None, layout="chw", max_ctas=0):
         """Enqueue one batch decode on `stream`; returns (status, bad_unit) device views.
         wide: performance hint for u8 batches of large images (policy N = 128), see l3.h.
         crops: optional int32 [n, 5] device tensor {y, x, h, w, flip}: decode only that window.
-        layout: "chw" (planar, default) or "hwc" (interleaved, L3_DECODE_LAYOUT_HWC)."""
+        layout: "chw" (planar, default) or "hwc" (interleaved, L3_DECODE_LAYOUT_HWC).
+        max_ctas: cap on the decoder's thread blocks (0 = every SM), to leave SMs to compute."""
         a = self.args(src, src_offsets, shapes, out, out_offsets=out_offsets, scale=scale, bias=bias, wide=wide,
-                      crops=crops, layout=layout)
+                      crops=crops, layout=layout, max_ctas=max_ctas)
         l3.l3_decode_batch(a, stream)
         n = int(shapes.shape[0])
         return self.status[:n], self.bad_unit[:n]
@@ -127,48 +129,53 @@ def encode_batch(images: Sequence[np.ndarray] | Sequence[torch.Tensor], patch_si
 class PipelinedLoader:
     """Load + decode pipeline (SURVEY.md §8(f1); PAPER.md:67 Load stage, :189 "we allocate both
     processes to separate CUDA streams. We prioritize the computing stream over the decoding
-    stream"). Batch i+1's compressed bytes move host -> HBM on a copy stream while batch i decodes
-    on a decode stream; both streams get the LOWEST priority so a training step on a
-    high-priority compute stream is not delayed by them. Double-buffered device staging.
+    stream"). Every batch goes through ONE C-ABI call with host buffers, l3_load_decode_batch:
+    pinned host bytes -> HBM, the decode kernel, statuses -> pinned host, all on one stream.
+    Consecutive batches alternate over `depth` streams, each with its own device staging buffer
+    and workspace, so batch i+1's host-to-device copy overlaps batch i's decode. The streams get
+    the LOWEST priority, so a training step on a high-priority compute stream is scheduled first;
+    `max_ctas` can further cap the decoder's thread blocks (l3.h) to leave SMs to compute.
 
-    submit() enqueues one batch (pinned host bytes) and returns the (status, out) it will fill;
-    the host copy of the statuses of batch i is readable after `wait(i)`."""
+    submit() enqueues one batch and returns a ticket; wait(ticket) blocks until that batch is
+    done and returns its host statuses. With the internal status buffers a ticket must be waited
+    for before `depth` more batches are submitted (its slot is then reused; wait raises); pass
+    host_status= (pinned, >= n int32) to keep every batch's statuses."""
 
-    def __init__(self, max_n: int, max_bytes: int, depth: int = 2, device="cuda"):
-        lo, _hi = torch.cuda.Stream.priority_range()
+    def __init__(self, max_n: int, max_bytes: int, depth: int = 2, device="cuda", max_ctas: int = 0):
+        lowest, _highest = torch.cuda.Stream.priority_range()
         self.device = torch.device(device)
-        self.copy_stream = torch.cuda.Stream(device=self.device, priority=lo)
-        self.decode_stream = torch.cuda.Stream(device=self.device, priority=lo)
+        self.depth = depth
+        self.max_ctas = max_ctas
+        self.streams = [torch.cuda.Stream(device=self.device, priority=lowest) for _ in range(depth)]
         self.stage = [torch.empty(max_bytes + 16, dtype=torch.uint8, device=self.device) for _ in range(depth)]
         self.dec = [BatchDecoder(max_n, self.device) for _ in range(depth)]
-        self.copied = [torch.cuda.Event() for _ in range(depth)]
-        self.freed = [torch.cuda.Event() for _ in range(depth)]
         self.host_status = [torch.empty(max_n, dtype=torch.int32).pin_memory() for _ in range(depth)]
         self.done = [torch.cuda.Event() for _ in range(depth)]
+        self.owner = [-1] * depth
         self.i = 0
 
     def submit(self, host_src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor, out: torch.Tensor,
-               *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), wide=False) -> int:
-        b = self.i % len(self.stage)
-        nbytes = host_src.numel()
-        with torch.cuda.stream(self.copy_stream):
-            if self.i >= len(self.stage):
-                self.copy_stream.wait_event(self.freed[b])          # staging buffer b no longer read
-            self.stage[b][:nbytes].copy_(host_src, non_blocking=True)
-            self.copied[b].record(self.copy_stream)
-        self.decode_stream.wait_event(self.copied[b])
+               *, out_offsets=None, scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), wide=False,
+               host_status: torch.Tensor | None = None) -> int:
+        b = self.i % self.depth
         n = int(shapes.shape[0])
+        if host_src.numel() > self.stage[b].numel():
+            raise ValueError("batch larger than the loader's staging buffers")
+        hs = self.host_status[b] if host_status is None else host_status
         a = self.dec[b].args(self.stage[b], src_offsets, shapes, out, out_offsets=out_offsets, scale=scale,
-                             bias=bias, wide=wide)
-        l3.l3_decode_batch(a, self.decode_stream)
-        self.freed[b].record(self.decode_stream)
-        with torch.cuda.stream(self.decode_stream):
-            self.host_status[b][:n].copy_(self.dec[b].status[:n], non_blocking=True)
-        self.done[b].record(self.decode_stream)
+                             bias=bias, wide=wide, max_ctas=self.max_ctas)
+        l3.l3_load_decode_batch(a, host_src, hs[:n], self.streams[b])
+        self.done[b].record(self.streams[b])
+        self.owner[b] = self.i
         self.i += 1
         return self.i - 1
 
     def wait(self, ticket: int) -> torch.Tensor:
-        b = ticket % len(self.stage)
+        """Block until batch `ticket` is decoded; returns the internal host status buffer of its slot
+        (only meaningful if the batch was submitted without host_status=)."""
+        b = ticket % self.depth
+        if self.owner[b] != ticket:
+            raise RuntimeError(f"ticket {ticket}: its slot was reused by ticket {self.owner[b]}; wait earlier "
+                               f"or pass host_status= to submit")
         self.done[b].synchronize()
         return self.host_status[b]

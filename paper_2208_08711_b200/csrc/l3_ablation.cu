@@ -63,7 +63,7 @@ __device__ __forceinline__ bool abl_unit(const AblParams& p, int img, uint32_t u
   const uint8_t* file = p.src + d.file_off;
   const uint64_t off = abl_u32le(file + 13 + 4ull * u);
   const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)abl_u32le(file + 17 + 4ull * u) : d.data_len;
-  if (nxt <= off || off >= d.data_len) return false;
+  if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) return false;
   const uint32_t ch = u / d.P, pp = u % d.P;
   U.data = p.src + d.data_off + off;
   U.len = nxt - off;

@@ -17,7 +17,9 @@
 // DESIGN.md §5 explains the mapping and its roofline.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 
 #include "l3_internal.cuh"
 
@@ -329,7 +331,7 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
   int lo = 0, hi = ga.n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
+    if (__ldcg(&prefix[mid]) <= task) lo = mid; else hi = mid;
   }
   const int img = lo;
   const ImgDesc d = ga.desc[img];
@@ -349,7 +351,7 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
   }
   const uint64_t off = ld_u32le(file + 13 + 4ull * u);
   const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
-  if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
+  if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
     if (lane == 0) atomicMin(&ga.errkey[img], 0u);   // header-level: CORRUPT_HEADER
     return phase_bits;
   }
@@ -563,9 +565,18 @@ cudaError_t launch_selftest_paeth4(uint8_t* out, cudaStream_t s) {
 }
 
 // ============================================================== host launch
-static int g_sm_count = 0;
-// f32, u8 narrow, u8 wide, f32 crop, u8 crop, f32 wide, f32 HWC tile, u8 HWC tile, f32 crop HWC, u8 crop HWC
-static int g_occ[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// Per-device launch geometry: SM count and resident CTAs per SM of every kernel variant, filled
+// once per device under a mutex (a first call racing from two threads must not see a
+// half-filled entry), read lock-free afterwards through the `ready` flag (release / acquire).
+enum Variant { kF32 = 0, kU8, kU8Wide, kF32Crop, kU8Crop, kF32HwcTile, kU8HwcTile, kF32CropHwc, kU8CropHwc, kVariants };
+struct DeviceInfo {
+  int sm_count = 0;
+  int occ[kVariants] = {};
+  std::atomic<bool> ready{false};
+};
+constexpr int kMaxDevices = 64;
+static DeviceInfo g_dev[kMaxDevices];
+static std::mutex g_dev_mu;
 
 template <bool F32, bool WIDE, bool CROP, bool HWC = false>
 static int fused_occupancy() {
@@ -585,24 +596,33 @@ static int hwc_occupancy() {
   return occ > 0 ? occ : 1;
 }
 
-cudaError_t ensure_device_info() {
-  if (g_sm_count == 0) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return e;
-    g_occ[0] = fused_occupancy<true, false, false>();
-    g_occ[1] = fused_occupancy<false, false, false>();
-    g_occ[2] = fused_occupancy<false, true, false>();
-    g_occ[3] = fused_occupancy<true, false, true>();
-    g_occ[4] = fused_occupancy<false, false, true>();
-    g_occ[5] = fused_occupancy<true, true, false>();
-    g_occ[6] = hwc_occupancy<true>();
-    g_occ[7] = hwc_occupancy<false>();
-    g_occ[8] = fused_occupancy<true, false, true, true>();
-    g_occ[9] = fused_occupancy<false, false, true, true>();
+// The calling thread's current device's entry (filled on first use).
+cudaError_t device_info(const DeviceInfo** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  DeviceInfo& di = g_dev[dev];
+  if (!di.ready.load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!di.ready.load(std::memory_order_relaxed)) {
+      e = cudaDeviceGetAttribute(&di.sm_count, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return e;
+      di.occ[kF32] = fused_occupancy<true, false, false>();
+      di.occ[kU8] = fused_occupancy<false, false, false>();
+      di.occ[kU8Wide] = fused_occupancy<false, true, false>();
+      di.occ[kF32Crop] = fused_occupancy<true, false, true>();
+      di.occ[kU8Crop] = fused_occupancy<false, false, true>();
+      di.occ[kF32HwcTile] = hwc_occupancy<true>();
+      di.occ[kU8HwcTile] = hwc_occupancy<false>();
+      di.occ[kF32CropHwc] = fused_occupancy<true, false, true, true>();
+      di.occ[kU8CropHwc] = fused_occupancy<false, false, true, true>();
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      di.ready.store(true, std::memory_order_release);
+    }
   }
+  *out = &di;
   return cudaSuccess;
 }
 
@@ -629,9 +649,11 @@ cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_va
   return cudaGetLastError();
 }
 
-// The whole hot path in ONE persistent launch (grid = SMs x resident CTAs).
+// The whole hot path in ONE persistent launch (grid = SMs x resident CTAs, or fewer CTAs when the
+// caller caps the decoder's share of the GPU with max_ctas, l3.h).
 cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
-  cudaError_t e = ensure_device_info();
+  const DeviceInfo* di = nullptr;
+  cudaError_t e = device_info(&di);
   if (e != cudaSuccess) return e;
   DecodeParams dp;
   dp.pp = make_parse_params(a);
@@ -642,37 +664,39 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   }
   dp.key_scale = 128u;
   const bool f32 = a->out_kind == L3_OUT_F32;
-  // f3: full-image HWC -> the tile kernel; crop window / flip (CHW or HWC) -> the augment variant
-  if ((a->flags & L3_DECODE_LAYOUT_HWC) && a->crops == nullptr) {
-    const int v = f32 ? 6 : 7;
-    const int grid = g_sm_count * g_occ[v];
+  const bool crop = a->crops != nullptr;
+  const bool hwc = (a->flags & L3_DECODE_LAYOUT_HWC) != 0;
+  // f3: full-image HWC -> the tile kernel; crop window / flip (CHW or HWC) -> the augment variant;
+  // the wide 8-column path is a u8-only hint (l3.h)
+  const bool tile = hwc && !crop;
+  const bool wide = !crop && !f32 && (a->flags & L3_DECODE_HINT_WIDE);
+  const Variant v = tile ? (f32 ? kF32HwcTile : kU8HwcTile)
+                    : crop ? (hwc ? (f32 ? kF32CropHwc : kU8CropHwc) : (f32 ? kF32Crop : kU8Crop))
+                           : (f32 ? kF32 : (wide ? kU8Wide : kU8));
+  int ctas = di->occ[v];
+  if (const char* ev = getenv("L3_DEV_CTAS_PER_SM")) {   // dev-only A/B of the persistent grid
+    const int x = atoi(ev);
+    if (x > 0 && x < ctas) ctas = x;
+  }
+  int grid = di->sm_count * ctas;
+  if (a->max_ctas > 0 && (int)a->max_ctas < grid) grid = (int)a->max_ctas;
+  dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
+  dp.pp.wide = wide ? 1u : 0u;
+  if (tile) {
     if (f32) l3_decode_hwc_kernel<true><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
     else l3_decode_hwc_kernel<false><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
     return cudaGetLastError();
   }
-  const bool crop = a->crops != nullptr;
-  const bool crop_hwc = crop && (a->flags & L3_DECODE_LAYOUT_HWC);
-  const bool wide = !crop && (a->flags & L3_DECODE_HINT_WIDE);
-  const int variant = crop_hwc ? (f32 ? 8 : 9) : crop ? (f32 ? 3 : 4) : (f32 ? (wide ? 5 : 0) : (wide ? 2 : 1));
-  int ctas = g_occ[variant];
-  if (const char* e = getenv("L3_DEV_CTAS_PER_SM")) {   // dev-only A/B of the persistent grid
-    const int v = atoi(e);
-    if (v > 0 && v < ctas) ctas = v;
-  }
-  const int grid = g_sm_count * ctas;
-  dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
-  dp.pp.wide = wide ? 1u : 0u;
   const size_t smem = fast_smem_bytes();
   const dim3 B(kWarpsPerCta * 32);
-  switch (variant) {
-    case 0: l3_decode_kernel<true, false, false><<<grid, B, smem, s>>>(dp); break;
-    case 1: l3_decode_kernel<false, false, false><<<grid, B, smem, s>>>(dp); break;
-    case 2: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
-    case 3: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
-    case 4: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
-    case 8: l3_decode_kernel<true, false, true, true><<<grid, B, smem, s>>>(dp); break;
-    case 9: l3_decode_kernel<false, false, true, true><<<grid, B, smem, s>>>(dp); break;
-    default: l3_decode_kernel<true, true, false><<<grid, B, smem, s>>>(dp); break;
+  switch (v) {
+    case kF32: l3_decode_kernel<true, false, false><<<grid, B, smem, s>>>(dp); break;
+    case kU8: l3_decode_kernel<false, false, false><<<grid, B, smem, s>>>(dp); break;
+    case kU8Wide: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
+    case kF32Crop: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
+    case kU8Crop: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
+    case kF32CropHwc: l3_decode_kernel<true, false, true, true><<<grid, B, smem, s>>>(dp); break;
+    default: l3_decode_kernel<false, false, true, true><<<grid, B, smem, s>>>(dp); break;
   }
   return cudaGetLastError();
 }

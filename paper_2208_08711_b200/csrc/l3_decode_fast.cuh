@@ -31,6 +31,63 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   return v;
 }
 
+// ---------------------------------------------------------------- a1 / a7 inside the persistent launch
+// a1 election: the FIRST CTA of the launch to take the workspace's arrival ticket parses the
+// headers ("first reads the header of each image and then splits it into multiple
+// patches") and publishes the work decomposition with a release store; every other CTA waits
+// for it with acquire loads. The parser is resident by construction (it is running when it
+// takes ticket 0), so the waiting CTAs can never starve it, whatever order the CTAs are
+// dispatched in and whatever other kernels hold SMs at the time.
+__device__ __forceinline__ bool a1_elected(WsHead* head, unsigned int* sh_role) {
+  if (threadIdx.x == 0) *sh_role = atomicAdd(&head->arrived, 1u);
+  __syncthreads();
+  return *sh_role == 0u;
+}
+__device__ __forceinline__ void a1_publish(WsHead* head) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
+}
+__device__ __forceinline__ void a1_wait(WsHead* head) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire_gpu(&head->ready) == 0u) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
+// a7: the last CTA to finish converts the per-image error keys (atomicMin over the units,
+// key 0 = header-level error, else 1<<31 | unit<<1 | truncated) into status / bad_unit, the
+// result of a sequential decode, and re-zeroes the workspace head so
+// the next launch on this workspace needs no host work.
+__device__ __forceinline__ void a7_finish(const ParseParams& pp, WsHead* head, unsigned int* sh_ticket) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *sh_ticket = atomicAdd(&head->done_ctas, 1u);
+  }
+  __syncthreads();
+  if (*sh_ticket != gridDim.x - 1) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < pp.n; i += blockDim.x) {
+    if (pp.status[i] != L3_OK) continue;   // header-level error from a1
+    const uint32_t key = atomicAdd(&pp.ws.errkey[i], 0u);
+    if (key == kNoError) continue;
+    if (key == 0u) {
+      pp.status[i] = L3_E_CORRUPT_HEADER;
+    } else {
+      pp.status[i] = (key & 1u) ? L3_E_TRUNCATED_STREAM : L3_E_CORRUPT_STREAM;
+      if (pp.bad_unit) pp.bad_unit[i] = (int32_t)((key >> 1) & 0x3FFFFFFFu);
+    }
+  }
+  if (threadIdx.x == 0) {
+    head->next_task[0] = 0;
+    head->next_task[1] = 0;
+    head->done_ctas = 0;
+    head->ready = 0;
+    head->arrived = 0;
+  }
+}
+
 __host__ __device__ constexpr size_t fast_smem_bytes() {
   return (size_t)kWarpsPerCta * kRingPitch + (size_t)kWarpsPerCta * kSlots * 8 + 16;
 }
@@ -494,19 +551,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
   uint32_t phase_bits = 0;
   WsHead* head = p.pp.ws.head;
 
-  // ---- a1 inside the persistent launch: CTA 0 parses every header and
-  // publishes the work decomposition; the other CTAs wait on the ready flag
-  // (CTA 0 is dispatched first, so the wait cannot starve it).
-  if (blockIdx.x == 0) {
+  // ---- a1 inside the persistent launch: the first CTA to arrive parses every header
+  // and publishes the work decomposition; the other CTAs wait on the ready flag
+  if (a1_elected(head, &ticket)) {
     parse_phase<WIDE, HWC>(p.pp, sh_a, sh_b);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
+    a1_publish(head);
   } else {
-    if (threadIdx.x == 0) {
-      while (ld_acquire_gpu(&head->ready) == 0u) __nanosleep(64);
-    }
-    __syncthreads();
+    a1_wait(head);
   }
 
   const uint64_t* prefix = p.pp.ws.prefix[0];
@@ -538,7 +589,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
 #endif
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
+      if (__ldcg(&prefix[mid]) <= task) lo = mid; else hi = mid;
     }
     const int img = lo;
     const ImgDesc d = p.pp.ws.desc[img];
@@ -583,7 +634,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
     if (active) {
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
-      if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
+      if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
         if (j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
         active = false;
       } else {
@@ -753,34 +804,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
     }
   }
 
-  // ---- a7: per-image status, by the last CTA; it also re-zeroes the head so
-  // the workspace is ready for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    ticket = atomicAdd(&head->done_ctas, 1u);
-  }
-  __syncthreads();
-  if (ticket == gridDim.x - 1) {
-    __threadfence();
-    for (int i = threadIdx.x; i < p.pp.n; i += blockDim.x) {
-      if (p.pp.status[i] != L3_OK) continue;   // header-level error from a1
-      const uint32_t key = atomicAdd(&p.pp.ws.errkey[i], 0u);
-      if (key == kNoError) continue;
-      if (key == 0u) {
-        p.pp.status[i] = L3_E_CORRUPT_HEADER;
-      } else {
-        p.pp.status[i] = (key & 1u) ? L3_E_TRUNCATED_STREAM : L3_E_CORRUPT_STREAM;
-        if (p.pp.bad_unit) p.pp.bad_unit[i] = (int32_t)((key >> 1) & 0x3FFFFFFFu);
-      }
-    }
-    if (threadIdx.x == 0) {
-      head->next_task[0] = 0;
-      head->next_task[1] = 0;
-      head->done_ctas = 0;
-      head->ready = 0;
-    }
-  }
+  // ---- a7: per-image status, by the last CTA
+  a7_finish(p.pp, head, &ticket);
 }
 
 }  // namespace l3

@@ -189,7 +189,7 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
       off = ld_u32le(file + 13 + 4ull * u);
       nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
     }
-    act[c] = tact && !((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off));
+    act[c] = tact && !(unit_offsets_bad(u, nunits, off, nxt, d.data_len));
     if (tact && !act[c] && j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
     start[c] = act[c] ? d.data_off + off : 0;
     end[c] = act[c] ? d.data_off + nxt : 0;
@@ -318,16 +318,11 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
   WsHead* head = p.pp.ws.head;
 
   // a1 inside the launch (as in l3_decode_kernel): tasks = tiles for N <= 128
-  if (blockIdx.x == 0) {
+  if (a1_elected(head, &ticket)) {
     parse_phase_simple<false, true, true>(p.pp, sh_a, sh_b);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
+    a1_publish(head);
   } else {
-    if (threadIdx.x == 0) {
-      while (ld_acquire_gpu(&head->ready) == 0u) __nanosleep(64);
-    }
-    __syncthreads();
+    a1_wait(head);
   }
 
   const uint64_t* prefix = p.pp.ws.prefix[0];
@@ -343,7 +338,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     int lo = 0, hi = p.pp.n;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (__ldg(&prefix[mid]) <= task) lo = mid; else hi = mid;
+      if (__ldcg(&prefix[mid]) <= task) lo = mid; else hi = mid;
     }
     const int img = lo;
     const ImgDesc d = p.pp.ws.desc[img];
@@ -372,7 +367,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
       const uint32_t u = (uint32_t)c * d.P + pp;
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
-      act[c] = !((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off));
+      act[c] = !(unit_offsets_bad(u, nunits, off, nxt, d.data_len));
       if (!act[c] && lane == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
       start[c] = act[c] ? d.data_off + off : 0;
       end[c] = act[c] ? d.data_off + nxt : 0;
@@ -469,32 +464,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
   }
 
   // a7: per-image status by the last CTA, which also re-zeroes the workspace head
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    ticket = atomicAdd(&head->done_ctas, 1u);
-  }
-  __syncthreads();
-  if (ticket == gridDim.x - 1) {
-    __threadfence();
-    for (int i = threadIdx.x; i < p.pp.n; i += blockDim.x) {
-      if (p.pp.status[i] != L3_OK) continue;
-      const uint32_t key = atomicAdd(&p.pp.ws.errkey[i], 0u);
-      if (key == kNoError) continue;
-      if (key == 0u) {
-        p.pp.status[i] = L3_E_CORRUPT_HEADER;
-      } else {
-        p.pp.status[i] = (key & 1u) ? L3_E_TRUNCATED_STREAM : L3_E_CORRUPT_STREAM;
-        if (p.pp.bad_unit) p.pp.bad_unit[i] = (int32_t)((key >> 1) & 0x3FFFFFFFu);
-      }
-    }
-    if (threadIdx.x == 0) {
-      head->next_task[0] = 0;
-      head->next_task[1] = 0;
-      head->done_ctas = 0;
-      head->ready = 0;
-    }
-  }
+  a7_finish(p.pp, head, &ticket);
 }
 
 }  // namespace l3

@@ -329,7 +329,7 @@ __device__ __forceinline__ uint32_t decode_task8(const DecodeParams& p, const Im
     h = min(d.N, d.H - y0);
     const uint64_t off = ld_u32le(file + 13 + 4ull * u);
     const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
-    if ((u == 0 && off != 0) || off >= d.data_len || (u + 1 < nunits && nxt <= off)) {
+    if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
       if (j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
       active = false;
     } else {

@@ -46,8 +46,9 @@ static_assert(sizeof(ImgDesc) == 96, "ImgDesc");
 struct WsHead {
   unsigned long long next_task[2];   // dynamic schedulers: [0] N <= 128, [1] N > 128
   unsigned int done_ctas;            // last-CTA ticket
-  unsigned int ready;                // 1 once CTA 0 has published the a1 results of this launch
-  unsigned int pad[58];
+  unsigned int ready;                // 1 once the parsing CTA has published the a1 results of this launch
+  unsigned int arrived;              // arrival ticket: the first CTA to take it parses (a1)
+  unsigned int pad[57];
 };
 static_assert(sizeof(WsHead) == 256, "WsHead");
 
@@ -96,6 +97,16 @@ __host__ __device__ inline void lanes_and_group(uint32_t N, uint32_t* L, uint32_
   *L = l;
   *G = g;
   *mode = 0;
+}
+
+// Per-unit half of the a1 offset-table check (the oracle's
+// header rule): offsets start at 0, strictly increase over R||G||B and stay inside the data
+// section. Unit u checks its own offset and the next one, so a file truncated inside unit u's
+// data (off[u+1] >= data_len) is CORRUPT_HEADER for unit u too: its byte range would otherwise
+// run past the file (and, for the last file of a batch, past the source buffer).
+__device__ __forceinline__ bool unit_offsets_bad(uint32_t u, uint32_t nunits, uint64_t off, uint64_t nxt,
+                                                 uint64_t data_len) {
+  return (u == 0 && off != 0) || off >= data_len || (u + 1 < nunits && (nxt <= off || nxt >= data_len));
 }
 
 // ---------------------------------------------------------------- PTX helpers

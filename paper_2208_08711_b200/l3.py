@@ -45,7 +45,7 @@ class l3_decode_args(ctypes.Structure):
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_uint64),
         ("flags", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32),
+        ("max_ctas", ctypes.c_uint32),
         ("crops", ctypes.c_void_p),
     ]
 
@@ -144,7 +144,8 @@ def _stream(stream) -> int:
 
 
 def make_decode_args(src, src_offsets, shapes, out, status, workspace, *, out_offsets=None, bad_unit=None,
-                     scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), flags=0, crops=None) -> l3_decode_args:
+                     scale=(1.0, 1.0, 1.0), bias=(0.0, 0.0, 0.0), flags=0, crops=None,
+                     max_ctas=0) -> l3_decode_args:
     a = l3_decode_args()
     a.src = _dev_ptr(src, "src", torch.uint8)
     a.src_offsets = _dev_ptr(src_offsets, "src_offsets", torch.int64)
@@ -166,6 +167,7 @@ def make_decode_args(src, src_offsets, shapes, out, status, workspace, *, out_of
     a.workspace_bytes = workspace.numel() * workspace.element_size()
     a.flags = int(flags)
     a.crops = _dev_ptr(crops, "crops", torch.int32)
+    a.max_ctas = int(max_ctas)
     return a
 
 

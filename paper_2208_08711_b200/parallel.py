@@ -48,6 +48,15 @@ def max_over_ranks(value: float) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float) -> float:
+    """Sum of a per-rank scalar (e.g. algorithmic bytes) over all ranks; identity without a process group."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device_for_backend())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def all_ranks_true(flag: bool) -> bool:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return bool(flag)

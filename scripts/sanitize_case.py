@@ -60,3 +60,40 @@ for files_v in ([l3ref.encode(im, N=N) for im, N in zip(vimgs, Ns)],
         l3.l3_decode_batch_ablation(a, mode)
         torch.cuda.synchronize()
         print("ablation", mode, dec.status[:4].tolist())
+
+# a file cut inside a unit's data as the LAST file of an exactly-sized source
+# buffer (its later offsets point past the data): CORRUPT_HEADER, and no read past the buffer
+# (the sanitizer test runs with PYTORCH_NO_CUDA_MEMORY_CACHING=1: every tensor is its own allocation)
+import struct  # noqa: E402
+
+
+def cut_inside_unit(f, u):
+    W, H, N = struct.unpack("<IIB", f[4:13])
+    P = (-(-W // N)) * (-(-H // N))
+    uo = np.frombuffer(f[13:13 + 12 * P], "<u4")
+    return f[:13 + 12 * P + (int(uo[u]) + int(uo[u + 1])) // 2 + 1]
+
+
+for N in (32, 64, 128, 200):
+    tf = cut_inside_unit(l3ref.encode(imgs[1], N=N), 1)
+    ts, to = pack_files([files[0], tf])
+    assert ts.numel() == int(to[-1])
+    tsh = shapes[[0, 1]].contiguous()
+    tsz = [imgs[0].size, imgs[1].size]
+    too = torch.tensor([0, tsz[0]], dtype=torch.int64, device="cuda")
+    tdec = BatchDecoder(2)
+    for dtype in (torch.uint8, torch.float32):
+        for wide, layout in ((False, "chw"), (True, "chw"), (False, "hwc")):
+            out = torch.zeros(sum(tsz), dtype=dtype, device="cuda")
+            st, b = tdec.decode(ts, to, tsh, out, out_offsets=too, wide=wide, layout=layout)
+            torch.cuda.synchronize()
+            assert st.tolist() == [0, 3], (N, dtype, wide, layout, st.tolist())
+    cr = torch.tensor([[0, 0, imgs[0].shape[1], imgs[0].shape[2], 0], [1, 2, 50, 60, 1]], dtype=torch.int32,
+                      device="cuda")
+    for layout in ("chw", "hwc"):
+        out = torch.zeros(sum(tsz), dtype=torch.uint8, device="cuda")
+        st, b = tdec.decode(ts, to, tsh, out, out_offsets=torch.tensor([0, 3 * 70 * 133], dtype=torch.int64,
+                                                                        device="cuda"), crops=cr, layout=layout)
+        torch.cuda.synchronize()
+        print("cut", N, layout, st.tolist())
+print("truncated-last cases ok")

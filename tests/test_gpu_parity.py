@@ -282,30 +282,6 @@ def test_device_predictor4_exhaustive_2_24():
                                    for i in bad[:8]])
 
 
-def test_pipelined_loader_matches_direct_decode():
-    """f1 loader: overlapped H2D + decode on low-priority streams gives the same pixels / statuses."""
-    from paper_2208_08711_b200.api import PipelinedLoader
-    imgs = [l3synth.natural(200, 300, s, 2.0) for s in range(6)]
-    files = [l3ref.encode(im) for im in imgs]
-    batches = [files[:3], files[3:]]
-    loader = PipelinedLoader(3, max(sum(map(len, b)) for b in batches), depth=2)
-    outs, tickets = [], []
-    for b in batches + batches:
-        offs = torch.tensor(np.cumsum([0] + [len(f) for f in b]), dtype=torch.int64, device="cuda")
-        host = torch.from_numpy(np.frombuffer(b"".join(b), np.uint8).copy()).pin_memory()
-        sh = torch.tensor([[200, 300]] * len(b), dtype=torch.int32, device="cuda")
-        out = torch.empty((len(b), 3, 200, 300), dtype=torch.uint8, device="cuda")
-        tickets.append(loader.submit(host, offs, sh, out))
-        outs.append(out)
-    for k, t in enumerate(tickets):
-        assert loader.wait(t)[:3].tolist() == [0, 0, 0]
-    torch.cuda.synchronize()
-    for k, out in enumerate(outs):
-        ref = imgs[:3] if k % 2 == 0 else imgs[3:]
-        for i in range(3):
-            assert np.array_equal(out[i].cpu().numpy(), ref[i])
-
-
 # ------------------------------------------------------------------ f3: partial decode (crop / flip)
 
 def _crop_decode(files, shapes, crops, dtype=torch.uint8, scale=(1, 1, 1), bias=(0, 0, 0), layout="chw",
