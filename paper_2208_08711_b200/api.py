@@ -137,7 +137,9 @@ class PipelinedLoader:
     `max_ctas` can further cap the decoder's thread blocks (l3.h) to leave SMs to compute.
 
     submit() enqueues one batch and returns a ticket; wait(ticket) blocks until that batch is
-    done and returns its host statuses. With the internal status buffers a ticket must be waited
+    done and returns its host statuses. The loader holds references to a batch's host and device
+    buffers until its slot is reused (the asynchronous copies are invisible to torch's allocators);
+    a submit that reuses a slot first waits for the slot's previous batch. With the internal status buffers a ticket must be waited
     for before `depth` more batches are submitted (its slot is then reused; wait raises); pass
     host_status= (pinned, >= n int32) to keep every batch's statuses."""
 
@@ -152,6 +154,7 @@ class PipelinedLoader:
         self.host_status = [torch.empty(max_n, dtype=torch.int32).pin_memory() for _ in range(depth)]
         self.done = [torch.cuda.Event() for _ in range(depth)]
         self.owner = [-1] * depth
+        self.keep = [None] * depth      # host buffers of the batch in flight on each slot
         self.i = 0
 
     def submit(self, host_src: torch.Tensor, src_offsets: torch.Tensor, shapes: torch.Tensor, out: torch.Tensor,
@@ -162,10 +165,15 @@ class PipelinedLoader:
         if host_src.numel() > self.stage[b].numel():
             raise ValueError("batch larger than the loader's staging buffers")
         hs = self.host_status[b] if host_status is None else host_status
+        if self.keep[b] is not None:
+            # the slot's previous batch must be done before its staging buffer, workspace and host
+            # buffers are reused (the copies run asynchronously, outside torch's pinned-memory tracking)
+            self.done[b].synchronize()
         a = self.dec[b].args(self.stage[b], src_offsets, shapes, out, out_offsets=out_offsets, scale=scale,
                              bias=bias, wide=wide, max_ctas=self.max_ctas)
         l3.l3_load_decode_batch(a, host_src, hs[:n], self.streams[b])
         self.done[b].record(self.streams[b])
+        self.keep[b] = (host_src, hs, src_offsets, shapes, out, out_offsets)
         self.owner[b] = self.i
         self.i += 1
         return self.i - 1
