@@ -171,6 +171,9 @@ class PipelinedLoader:
             self.done[b].synchronize()
         a = self.dec[b].args(self.stage[b], src_offsets, shapes, out, out_offsets=out_offsets, scale=scale,
                              bias=bias, wide=wide, max_ctas=self.max_ctas)
+        # the caller's device tensors (offsets, shapes, out) were produced on its current stream: the
+        # loader's non-blocking stream must not run ahead of that work
+        self.streams[b].wait_stream(torch.cuda.current_stream(self.device))
         l3.l3_load_decode_batch(a, host_src, hs[:n], self.streams[b])
         self.done[b].record(self.streams[b])
         self.keep[b] = (host_src, hs, src_offsets, shapes, out, out_offsets)

@@ -280,9 +280,13 @@ def test_pipelined_loader_matches_direct_decode():
     low-priority streams; same pixels / statuses as the oracle, per-ticket statuses kept."""
     imgs = [l3synth.natural(200, 300, s, 2.0) for s in range(6)]
     files = [l3ref.encode(im) for im in imgs]
-    bad = bytearray(files[4]); bad[13 + 12 * 70 + 40] &= 0x0F   # a stream fault in the second batch
+    bad = bytearray(files[4]); bad[13 + 12 * 70 + 40] &= 0x0F   # changes pixels (still a valid stream)
+    off5 = int.from_bytes(bad[13 + 4 * 5:17 + 4 * 5], "little")
+    bad[13 + 12 * 70 + off5] &= 0x0F                              # unit 5, row 0: k = 0 -> CORRUPT_STREAM
     files_b = [files[:3], [files[3], bytes(bad), files[5]]]
-    ref_st = [[0, 0, 0], [l3ref.decode(f, exp_shape=(200, 300))[0] for f in files_b[1]]]
+    # the oracle's decode of every file (the injected byte may change pixels without a stream error)
+    ref_dec = [[l3ref.decode(f, exp_shape=(200, 300)) for f in b] for b in files_b]
+    ref_st = [[r[0] for r in rb] for rb in ref_dec]
     loader = PipelinedLoader(3, max(sum(map(len, b)) for b in files_b), depth=2)
     hs = torch.full((4, 3), -1, dtype=torch.int32).pin_memory()
     outs = []
@@ -294,13 +298,13 @@ def test_pipelined_loader_matches_direct_decode():
         loader.submit(host, offs, sh, out, host_status=hs[k])
         outs.append(out)
     torch.cuda.synchronize()
+    assert ref_st[1][1] == l3ref.E_CORRUPT_STREAM
     for k in range(4):
         assert hs[k].tolist() == ref_st[k % 2]
     for k, out in enumerate(outs):
-        ref = imgs[:3] if k % 2 == 0 else imgs[3:]
         for i in range(3):
             if ref_st[k % 2][i] == 0:
-                assert np.array_equal(out[i].cpu().numpy(), ref[i])
+                assert np.array_equal(out[i].cpu().numpy(), ref_dec[k % 2][i][2]), (k, i)
     # internal status slots: waiting for a ticket whose slot was reused raises
     t0 = loader.submit(host, offs, sh, outs[-1])
     loader.submit(host, offs, sh, outs[-1])
