@@ -124,11 +124,13 @@ typedef struct {
 uint64_t l3_decode_workspace_size(int32_t n);
 
 /*
- * The whole hot path as ONE persistent kernel
- * launch, asynchronously on `stream`: header parse + work decomposition (by the
- * first thread block), then the patch decoder on every SM (staging, row-header
- * chain, delta unpack, row-parallel custom Paeth, store / fused normalise),
- * then the per-image status (by the last thread block).
+ * The whole hot path as two launches, asynchronously
+ * on `stream`: a one-block kernel parses the headers and decomposes the work (a1),
+ * and the persistent patch decoder on every SM (staging, row-header chain, delta
+ * unpack, row-parallel custom Paeth, store / fused normalise; a2-a6) is launched
+ * as its programmatic dependent: its blocks are resident and set up before a1 ends
+ * and start decoding as soon as a1's results are visible. The last decoder block
+ * writes the per-image status (a7).
  * The workspace must be zero-filled before its first use (e.g. cudaMemsetAsync);
  * every call leaves it zero-filled again, so it can be reused without host work.
  */

@@ -31,7 +31,7 @@ extern "C" {
 
 uint64_t l3_decode_workspace_size(int32_t n) { return n < 0 ? 0 : l3::WsView::bytes(n); }
 
-int32_t l3_decode_kernels_per_call(void) { return 1; }
+int32_t l3_decode_kernels_per_call(void) { return 2; }
 
 l3_status_t l3_parse_batch(const l3_decode_args* a, l3_stream_t stream) {
   l3_status_t st = check_decode_args(a);

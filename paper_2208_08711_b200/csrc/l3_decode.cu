@@ -257,6 +257,26 @@ __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b
   }
 }
 
+// Programmatic dependent launch (PDL): the a1 kernel lets the decode grid launch at once
+// (launch_dependents); the decode grid's CTAs set up their rings, then block in
+// griddepcontrol.wait until a1 has completed and its descriptors / prefixes are visible. No
+// inter-CTA handshake, no spinning on a flag in L2.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+constexpr int kPrepThreads = 256;
+
+// a1 of a decode call, one CTA, followed by the decode grid (PDL): the work decomposition of the
+// decode kernel variant it precedes (WIDE: tail zone; AUG: crop / HWC descriptor bits; HWCK: the
+// HWC tile kernel's one task per (image, patch)).
+template <bool WIDE, bool AUG, bool HWCK>
+__global__ void __launch_bounds__(kPrepThreads) l3_prep_kernel(ParseParams p) {
+  pdl_launch_dependents();
+  __shared__ uint64_t sh_a[33], sh_b[33];
+  if (HWCK) parse_phase_simple<false, true, true>(p, sh_a, sh_b);
+  else parse_phase<WIDE, AUG>(p, sh_a, sh_b);
+}
+
 // Standalone a1 (l3_parse_batch): header validation and work decomposition only.
 // VARIANT: the ablation decoders' parse, which also accepts "L3IP" (reading C16).
 template <bool VARIANT>
@@ -682,23 +702,38 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   if (a->max_ctas > 0 && (int)a->max_ctas < grid) grid = (int)a->max_ctas;
   dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
   dp.pp.wide = wide ? 1u : 0u;
+  // launch 1: a1 (one CTA); launch 2: the persistent decode grid, programmatically dependent on it
+  if (tile) l3_prep_kernel<false, true, true><<<1, kPrepThreads, 0, s>>>(dp.pp);
+  else if (wide) l3_prep_kernel<true, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
+  else if (crop && hwc) l3_prep_kernel<false, true, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
+  else l3_prep_kernel<false, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (tile) {
-    if (f32) l3_decode_hwc_kernel<true><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
-    else l3_decode_hwc_kernel<false><<<grid, kHwcWarps * 32, hwc_smem_bytes(), s>>>(dp);
-    return cudaGetLastError();
+    cfg.blockDim = dim3(kHwcWarps * 32);
+    cfg.dynamicSmemBytes = hwc_smem_bytes();
+    return f32 ? cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<true>, dp)
+               : cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<false>, dp);
   }
-  const size_t smem = fast_smem_bytes();
-  const dim3 B(kWarpsPerCta * 32);
+  cfg.blockDim = dim3(kWarpsPerCta * 32);
+  cfg.dynamicSmemBytes = fast_smem_bytes();
   switch (v) {
-    case kF32: l3_decode_kernel<true, false, false><<<grid, B, smem, s>>>(dp); break;
-    case kU8: l3_decode_kernel<false, false, false><<<grid, B, smem, s>>>(dp); break;
-    case kU8Wide: l3_decode_kernel<false, true, false><<<grid, B, smem, s>>>(dp); break;
-    case kF32Crop: l3_decode_kernel<true, false, true><<<grid, B, smem, s>>>(dp); break;
-    case kU8Crop: l3_decode_kernel<false, false, true><<<grid, B, smem, s>>>(dp); break;
-    case kF32CropHwc: l3_decode_kernel<true, false, true, true><<<grid, B, smem, s>>>(dp); break;
-    default: l3_decode_kernel<false, false, true, true><<<grid, B, smem, s>>>(dp); break;
+    case kF32: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<true, false, false>, dp);
+    case kU8: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, false, false>, dp);
+    case kU8Wide: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, true, false>, dp);
+    case kF32Crop: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<true, false, true>, dp);
+    case kU8Crop: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, false, true>, dp);
+    case kF32CropHwc: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<true, false, true, true>, dp);
+    default: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, false, true, true>, dp);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace l3

@@ -31,30 +31,7 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   return v;
 }
 
-// ---------------------------------------------------------------- a1 / a7 inside the persistent launch
-// a1 election: the FIRST CTA of the launch to take the workspace's arrival ticket parses the
-// headers ("first reads the header of each image and then splits it into multiple
-// patches") and publishes the work decomposition with a release store; every other CTA waits
-// for it with acquire loads. The parser is resident by construction (it is running when it
-// takes ticket 0), so the waiting CTAs can never starve it, whatever order the CTAs are
-// dispatched in and whatever other kernels hold SMs at the time.
-__device__ __forceinline__ bool a1_elected(WsHead* head, unsigned int* sh_role) {
-  if (threadIdx.x == 0) *sh_role = atomicAdd(&head->arrived, 1u);
-  __syncthreads();
-  return *sh_role == 0u;
-}
-__device__ __forceinline__ void a1_publish(WsHead* head) {
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release_gpu(&head->ready, 1u);
-}
-__device__ __forceinline__ void a1_wait(WsHead* head) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire_gpu(&head->ready) == 0u) __nanosleep(64);
-  }
-  __syncthreads();
-}
-
+// ---------------------------------------------------------------- a7 inside the persistent launch
 // a7: the last CTA to finish converts the per-image error keys (atomicMin over the units,
 // key 0 = header-level error, else 1<<31 | unit<<1 | truncated) into status / bad_unit, the
 // result of a sequential decode, and re-zeroes the workspace head so
@@ -83,8 +60,6 @@ __device__ __forceinline__ void a7_finish(const ParseParams& pp, WsHead* head, u
     head->next_task[0] = 0;
     head->next_task[1] = 0;
     head->done_ctas = 0;
-    head->ready = 0;
-    head->arrived = 0;
   }
 }
 
@@ -538,7 +513,6 @@ template <bool F32, bool WIDE, bool CROP, bool HWC = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_MIN_CTAS))
     l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t sh_a[33], sh_b[33];
   __shared__ unsigned int ticket;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * kRingPitch;
@@ -551,14 +525,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
   uint32_t phase_bits = 0;
   WsHead* head = p.pp.ws.head;
 
-  // ---- a1 inside the persistent launch: the first CTA to arrive parses every header
-  // and publishes the work decomposition; the other CTAs wait on the ready flag
-  if (a1_elected(head, &ticket)) {
-    parse_phase<WIDE, HWC>(p.pp, sh_a, sh_b);
-    a1_publish(head);
-  } else {
-    a1_wait(head);
-  }
+  // ---- a1 ran in the preceding l3_prep_kernel (PDL): wait until its results are visible
+  pdl_wait();
 
   const uint64_t* prefix = p.pp.ws.prefix[0];
 #if L3_SMEM_PREFIX
@@ -574,9 +542,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
   const uint64_t lim = p.pp.src_offsets[p.pp.n] & ~15ull;
   const uint32_t K = p.key_scale;
 
-  uint64_t task = 0;
-  if (lane == 0) task = atomicAdd(&head->next_task[0], 1ull);
-  task = __shfl_sync(0xffffffffu, task, 0);
+  // the first task of every warp is its grid-wide warp index (no claim burst on the counter at the
+  // start); later tasks come from the dynamic counter, offset by the grid's warp count
+  const uint64_t grid_warps = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint64_t task = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   while (task < total_tasks) {
     int lo = 0, hi = p.pp.n;
 #if L3_SMEM_PREFIX
@@ -596,7 +565,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
     const uint32_t t = (uint32_t)(task - prefix[img]);
     // claim the next task now; the atomic's latency hides behind this one
     uint64_t next = 0;
-    if (lane == 0) next = atomicAdd(&head->next_task[0], 1ull);
+    if (lane == 0) next = grid_warps + atomicAdd(&head->next_task[0], 1ull);
 
     if (WIDE && (d.mode == 1 || d.mode == 2)) {   // u8 out, 33 <= N <= 128: wide 8-column lanes
       phase_bits = (d.mode == 1) ? decode_task8<F32, 4>(p, d, img, t, ring, bars, phase_bits, lim, K)

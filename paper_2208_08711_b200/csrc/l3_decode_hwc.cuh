@@ -304,7 +304,6 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
 template <bool F32>
 __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t sh_a[33], sh_b[33];
   __shared__ unsigned int ticket;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* rings = smem + warp * 3 * kHwcPitch;
@@ -317,13 +316,8 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
   uint32_t ph[3] = {0u, 0u, 0u};
   WsHead* head = p.pp.ws.head;
 
-  // a1 inside the launch (as in l3_decode_kernel): tasks = tiles for N <= 128
-  if (a1_elected(head, &ticket)) {
-    parse_phase_simple<false, true, true>(p.pp, sh_a, sh_b);
-    a1_publish(head);
-  } else {
-    a1_wait(head);
-  }
+  // a1 ran in the preceding l3_prep_kernel (PDL; tasks = tiles for N <= 128)
+  pdl_wait();
 
   const uint64_t* prefix = p.pp.ws.prefix[0];
   const uint64_t total_tasks = prefix[p.pp.n];
@@ -331,9 +325,8 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
   const uint32_t K = p.key_scale;
   const uint32_t esz = F32 ? 4u : 1u;
 
-  uint64_t task = 0;
-  if (lane == 0) task = atomicAdd(&head->next_task[0], 1ull);
-  task = __shfl_sync(0xffffffffu, task, 0);
+  const uint64_t grid_warps = (uint64_t)gridDim.x * kHwcWarps;   // first task: the grid-wide warp index
+  uint64_t task = (uint64_t)blockIdx.x * kHwcWarps + warp;
   while (task < total_tasks) {
     int lo = 0, hi = p.pp.n;
     while (hi - lo > 1) {
@@ -344,7 +337,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     const ImgDesc d = p.pp.ws.desc[img];
     const uint32_t pp = (uint32_t)(task - prefix[img]);   // patch index: the tile (mode 6: tile group)
     uint64_t next = 0;
-    if (lane == 0) next = atomicAdd(&head->next_task[0], 1ull);
+    if (lane == 0) next = grid_warps + atomicAdd(&head->next_task[0], 1ull);
     if (d.mode == 6) {   // N <= 32: G tiles per task, whole-staged
       ph[0] = hwc_small_task<F32>(p, d, img, pp, rings, bars, ph[0], lim, K, lane);
       task = __shfl_sync(0xffffffffu, next, 0);

@@ -46,9 +46,7 @@ static_assert(sizeof(ImgDesc) == 96, "ImgDesc");
 struct WsHead {
   unsigned long long next_task[2];   // dynamic schedulers: [0] N <= 128, [1] N > 128
   unsigned int done_ctas;            // last-CTA ticket
-  unsigned int ready;                // 1 once the parsing CTA has published the a1 results of this launch
-  unsigned int arrived;              // arrival ticket: the first CTA to take it parses (a1)
-  unsigned int pad[57];
+  unsigned int pad[59];
 };
 static_assert(sizeof(WsHead) == 256, "WsHead");
 

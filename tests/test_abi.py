@@ -65,7 +65,7 @@ def test_host_helpers(lib):
         assert l3.l3_encode_max_bytes(W, H, N) >= l3ref.max_file_bytes(W, H, N) - 3 * ((W + 7) * (H + 7))
     assert l3.l3_status_string(4) == "corrupt stream"
     assert l3.l3_decode_workspace_size(32) >= 32 * 64
-    assert l3.l3_decode_kernels_per_call() == 1
+    assert l3.l3_decode_kernels_per_call() == 2
 
 
 def test_no_cpu_fallback_without_cuda(lib):
