@@ -26,7 +26,7 @@ def main():
         dt = torch.float32 if out_kind == "f32" else torch.uint8
         out = torch.empty((n, 3, 1024, 2048), dtype=dt, device="cuda")
         dec = BatchDecoder(n)
-        a = dec.args(src, offs_t, shapes, out, scale=scale, bias=bias)
+        a = dec.args(src, offs_t, shapes, out, scale=scale, bias=bias, wide=os.environ.get('WIDE') == '1')
         for _ in range(3):
             l3.l3_decode_batch(a, stream)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
