@@ -129,6 +129,12 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
   if (3ull * P >= (uint64_t)kMaxUnitsPerImage || len < hdr) return L3_E_CORRUPT_HEADER;
   d.gx = (uint32_t)gx;
   d.P = (uint32_t)P;
+  // the sub-grid of patches a crop window touches (patches are independently addressable through the
+  // offset arrays): only these are decoded; without crops, the whole grid
+  d.px0 = p.crops ? d.cx / d.N : 0u;
+  d.py0 = p.crops ? d.cy / d.N : 0u;
+  d.gxw = p.crops ? (d.cx + d.cw - 1u) / d.N - d.px0 + 1u : (uint32_t)gx;
+  d.gyw = p.crops ? (d.cy + d.ch - 1u) / d.N - d.py0 + 1u : (uint32_t)gy;
   d.file_off = f0;
   d.data_off = f0 + hdr;
   d.data_len = len - hdr;
@@ -153,7 +159,10 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
           d.L = 32;
           d.G = 1;
         }
-        d.tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
+        // crop (f3): tasks only over the 3 x gxw x gyw units the window touches (modes 0 / 4);
+        // mode 3 (N > 128, generic path) walks every unit and skips
+        const uint64_t units = (p.crops && d.mode != 3) ? 3ull * d.gxw * d.gyw : 3ull * d.P;
+        d.tasks = (uint32_t)((units + d.G - 1) / d.G);
         if (HWCK && d.mode == 0) {   // N <= 32: G = 32 / L tiles (L-lane segments) per task
           d.mode = 6;
           d.G = 32u / d.L;

@@ -258,9 +258,9 @@ struct LaneRows {
   uint32_t selG;      // RAGGED: PRMT selector replicating column w-1 into the lane's ghost columns
   // CROP variant only (f3, partial decode): output window mapping
   int32_t ri;         // current image row - crop top
-  int32_t cj0;        // first column of this lane - crop left
-  uint32_t cw, chh;   // crop width / height
-  bool flip;          // horizontal flip of the window
+  uint32_t chh;       // crop height
+  uint32_t cmask;     // which of the lane's 4 output elements are inside the patch and the window
+  uint32_t qsel;      // PRMT selector putting the lane's samples in output order (flip: reversed)
 };
 
 // FAST: aligned vector store. Otherwise scalar stores; RAGGED: the patch width is not a multiple of
@@ -331,22 +331,23 @@ __device__ __forceinline__ void store4q(const LaneRows& s, uint32_t q, float sc,
   }
 }
 
-// f3: store the lane's 4 samples into a cropped (optionally flipped) window, planar or HWC.
+// f3: store the lane's 4 samples into a cropped (optionally flipped) window, planar or HWC. s.optr
+// walks the output row by row at the lane's lowest-address element (flip: the lane's 4 samples are
+// reversed into output order by the s.qsel PRMT), so the 4 elements sit at fixed immediate offsets;
+// s.cmask holds which of them are inside the patch and the window (fixed per task). Pair form
+// (xA, xB), or (BYTES) byte form [c0 c1 c2 c3] in xA.
 template <bool F32, bool HWC, bool BYTES = false>
 __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi,
-                                            bool pred) {
-  if (!pred || (uint32_t)s.ri >= s.chh) return;
-  // pair form (xA, xB), or (BYTES) byte form [c0 c1 c2 c3] in xA
-  const uint32_t x[4] = {BYTES ? (xA & 0xFFu) : (xA & 0xFFFFu), BYTES ? ((xA >> 8) & 0xFFu) : (xA >> 16),
-                         BYTES ? ((xA >> 16) & 0xFFu) : (xB & 0xFFFFu), BYTES ? (xA >> 24) : (xB >> 16)};
-  const uint64_t row = (uint64_t)(uint32_t)s.ri * s.cw;
+                                            bool live) {
+  constexpr uint32_t kStep = (HWC ? 3u : 1u) * (F32 ? 4u : 1u);   // bytes between the lane's elements
+  const bool rowok = live && (uint32_t)s.ri < s.chh;
+  const uint32_t qq = prmt(BYTES ? xA : prmt(xA, xB, 0x6420u), 0u, s.qsel);
 #pragma unroll
   for (int t = 0; t < 4; t++) {
-    const int32_t c = s.cj0 + t;
-    if (s.j4 + t < s.w && (uint32_t)c < s.cw) {
-      const uint64_t e = (row + (s.flip ? (s.cw - 1u - (uint32_t)c) : (uint32_t)c)) * (HWC ? 3u : 1u);
-      if (F32) reinterpret_cast<float*>(s.optr)[e] = fmaf((float)x[t], sc, bi);
-      else s.optr[e] = (uint8_t)x[t];
+    if (rowok && ((s.cmask >> t) & 1u)) {
+      const uint32_t x = (qq >> (8 * t)) & 0xFFu;
+      if (F32) *reinterpret_cast<float*>(s.optr + t * kStep) = fmaf((float)x, sc, bi);
+      else s.optr[t * kStep] = (uint8_t)x;
     }
   }
 }
@@ -401,7 +402,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     }
     uint32_t q = prmt(xA, xB, 0x6420u);   // [c0 c1 c2 c3] mod 256
     if (RAGGED) q = prmt(q, 0u, s.selG);  // columns >= w: ghosts of column w-1
-    if (CROP) store4_crop<F32, HWC, true>(s, q, 0u, sc, bi, live && s.valid);
+    if (CROP) store4_crop<F32, HWC, true>(s, q, 0u, sc, bi, live);
     else store4q<F32, FAST, RAGGED>(s, q, sc, bi, live && s.valid);
     s.Q = q;
   } else {
@@ -435,7 +436,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   // a6: store (u8 planar, or fused cast + normalise)
   if (!STORE) {
   } else if (CROP) {
-    store4_crop<F32, HWC>(s, xA, xB, sc, bi, live && s.valid);
+    store4_crop<F32, HWC>(s, xA, xB, sc, bi, live);
   } else {
     store4<F32, FAST, RAGGED>(s, xA, xB, sc, bi, live && s.valid);
   }
@@ -450,6 +451,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   if (!STORE) {
   } else if (CROP) {
     s.ri++;
+    s.optr += s.pitch;
   } else {
     s.optr += s.pitch;
   }
@@ -581,16 +583,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
     const uint32_t Lw = stream ? 32u : d.L;            // G == 1: the unit spans the warp
     const uint32_t seg = stream ? 0u : lane / Lw, j = stream ? (uint32_t)lane : lane % Lw;
     const uint32_t nunits = 3u * d.P;
-    const uint32_t u = t * G + seg;
+    const uint32_t v = t * G + seg;   // unit of the task's image (crop: among the window's units)
     const uint8_t* file = p.pp.src + d.file_off;
 
-    bool active = (seg < G) && (u < nunits);
-    uint32_t w = 0, h = 0, x0 = 0, y0 = 0, ch = 0;
+    bool active = (seg < G) && (v < (CROP ? 3u * d.gxw * d.gyw : nunits));
+    uint32_t w = 0, h = 0, x0 = 0, y0 = 0, ch = 0, u = v;
     uint64_t start = 0, end = 0;
     if (active) {
-      ch = u / d.P;
-      const uint32_t pp = u - ch * d.P;
-      const uint32_t px = pp % d.gx, py = pp / d.gx;
+      uint32_t px, py;
+      if (CROP) {   // f3: unit v of the touched sub-grid -> channel, patch
+        const uint32_t per = d.gxw * d.gyw;
+        ch = v / per;
+        const uint32_t rem = v - ch * per;
+        py = d.py0 + rem / d.gxw;
+        px = d.px0 + rem % d.gxw;
+        u = ch * d.P + py * d.gx + px;
+      } else {
+        ch = u / d.P;
+        const uint32_t pp = u - ch * d.P;
+        px = pp % d.gx;
+        py = pp / d.gx;
+      }
       x0 = px * d.N;
       y0 = py * d.N;
       w = min(d.N, d.W - x0);
@@ -634,14 +647,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
     s.selG = (w >= s.j4 + 4u) ? 0x3210u : (w == s.j4 + 3u) ? 0x2210u : (w == s.j4 + 2u) ? 0x1110u : 0x0000u;
     const uint32_t esz = F32 ? 4u : 1u;
     if (CROP) {   // augment variant (f3): window, flip; planar, or HWC (interleaved channels)
-      s.optr = reinterpret_cast<uint8_t*>(p.out) +
-               (d.out_off + (HWC ? (uint64_t)ch : (uint64_t)ch * d.ch * d.cw)) * esz;
-      s.pitch = 0;
+      const bool flip = HWC ? (d.flip & 1u) != 0 : d.flip != 0;
+      const int32_t cw = (int32_t)d.cw, cj0 = (int32_t)(x0 + s.j4) - (int32_t)d.cx;
+      const int32_t bc = flip ? cw - 4 - cj0 : cj0;   // window column of the lane's lowest-address element
+      const int64_t stride = (HWC ? 3 : 1) * (int64_t)esz;
       s.ri = (int32_t)y0 - (int32_t)d.cy;
-      s.cj0 = (int32_t)(x0 + s.j4) - (int32_t)d.cx;
-      s.cw = d.cw;
       s.chh = d.ch;
-      s.flip = HWC ? (d.flip & 1u) != 0 : d.flip != 0;
+      s.pitch = (uint32_t)(cw * stride);
+      s.optr = reinterpret_cast<uint8_t*>(p.out) +
+               (int64_t)(d.out_off + (HWC ? (uint64_t)ch : (uint64_t)ch * d.ch * d.cw)) * esz +
+               ((int64_t)s.ri * cw + bc) * stride;
+      s.qsel = flip ? 0x0123u : 0x3210u;
+      s.cmask = 0;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int32_t c = flip ? 3 - t : t;   // lane column of output slot t
+        if (active && s.j4 + (uint32_t)c < w && cj0 + c >= 0 && cj0 + c < cw) s.cmask |= 1u << t;
+      }
     } else {
       const uint64_t elem = d.out_off + (uint64_t)ch * d.W * d.H + (uint64_t)y0 * d.W + x0 + s.j4;
       s.optr = reinterpret_cast<uint8_t*>(p.out) + elem * esz;

@@ -36,9 +36,10 @@ struct ImgDesc {
   uint32_t mode;       // decode path: 0 whole-staged 4-column lanes (N <= 32), 1 / 2 wide 8-column
                        // lanes with 4 KB / 2 KB segment rings (65..128 / 33..64), 3 generic (N > 128)
   uint32_t cy, cx, ch, cw, flip;   // output window (crop) of the image: rows [cy, cy+ch), cols [cx, cx+cw)
+  uint32_t px0, py0, gxw, gyw;     // crop: the patches the window touches, [px0, px0+gxw) x [py0, py0+gyw)
   uint32_t pad_[2];
 };
-static_assert(sizeof(ImgDesc) == 96, "ImgDesc");
+static_assert(sizeof(ImgDesc) == 112, "ImgDesc");
 
 // Workspace layout (256-byte aligned sections).
 // Zero-filled before first use; every decode launch leaves it zero-filled again
