@@ -163,13 +163,14 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
         // mode 3 (N > 128, generic path) walks every unit and skips
         const uint64_t units = (p.crops && d.mode != 3) ? 3ull * d.gxw * d.gyw : 3ull * d.P;
         d.tasks = (uint32_t)((units + d.G - 1) / d.G);
+        const uint32_t tiles = p.crops ? d.gxw * d.gyw : d.P;   // crop: the tiles the window touches
         if (HWCK && d.mode == 0) {   // N <= 32: G = 32 / L tiles (L-lane segments) per task
           d.mode = 6;
           d.G = 32u / d.L;
-          d.tasks = (d.P + d.G - 1) / d.G;
+          d.tasks = (tiles + d.G - 1) / d.G;
         } else if (HWCK && d.mode != 3) {   // one tile per task, streamed
           d.mode = 5;
-          d.tasks = d.P;
+          d.tasks = tiles;
         }
         if (d.mode != 3) t0 = d.tasks; else t1 = d.tasks;
       } else {
@@ -617,11 +618,12 @@ static int fused_occupancy() {
   return occ > 0 ? occ : 1;
 }
 
-template <bool F32>
+template <bool F32, bool WIN>
 static int hwc_occupancy() {
   int occ = 0;
-  cudaFuncSetAttribute(l3_decode_hwc_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hwc_smem_bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_hwc_kernel<F32>, kHwcWarps * 32, hwc_smem_bytes());
+  cudaFuncSetAttribute(l3_decode_hwc_kernel<F32, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)hwc_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, l3_decode_hwc_kernel<F32, WIN>, kHwcWarps * 32, hwc_smem_bytes());
   return occ > 0 ? occ : 1;
 }
 
@@ -642,10 +644,10 @@ cudaError_t device_info(const DeviceInfo** out) {
       di.occ[kU8Wide] = fused_occupancy<false, true, false>();
       di.occ[kF32Crop] = fused_occupancy<true, false, true>();
       di.occ[kU8Crop] = fused_occupancy<false, false, true>();
-      di.occ[kF32HwcTile] = hwc_occupancy<true>();
-      di.occ[kU8HwcTile] = hwc_occupancy<false>();
-      di.occ[kF32CropHwc] = fused_occupancy<true, false, true, true>();
-      di.occ[kU8CropHwc] = fused_occupancy<false, false, true, true>();
+      di.occ[kF32HwcTile] = hwc_occupancy<true, false>();
+      di.occ[kU8HwcTile] = hwc_occupancy<false, false>();
+      di.occ[kF32CropHwc] = hwc_occupancy<true, true>();
+      di.occ[kU8CropHwc] = hwc_occupancy<false, true>();
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       di.ready.store(true, std::memory_order_release);
@@ -695,12 +697,12 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   const bool f32 = a->out_kind == L3_OUT_F32;
   const bool crop = a->crops != nullptr;
   const bool hwc = (a->flags & L3_DECODE_LAYOUT_HWC) != 0;
-  // f3: full-image HWC -> the tile kernel; crop window / flip (CHW or HWC) -> the augment variant;
+  // f3: HWC (full image or crop window) -> the tile kernel; crop window / flip CHW -> the augment variant;
   // the wide 8-column path is a u8-only hint (l3.h)
-  const bool tile = hwc && !crop;
+  const bool tile = hwc;
   const bool wide = !crop && !f32 && (a->flags & L3_DECODE_HINT_WIDE);
-  const Variant v = tile ? (f32 ? kF32HwcTile : kU8HwcTile)
-                    : crop ? (hwc ? (f32 ? kF32CropHwc : kU8CropHwc) : (f32 ? kF32Crop : kU8Crop))
+  const Variant v = tile ? (crop ? (f32 ? kF32CropHwc : kU8CropHwc) : (f32 ? kF32HwcTile : kU8HwcTile))
+                    : crop ? (f32 ? kF32Crop : kU8Crop)
                            : (f32 ? kF32 : (wide ? kU8Wide : kU8));
   int ctas = di->occ[v];
   if (const char* ev = getenv("L3_DEV_CTAS_PER_SM")) {   // dev-only A/B of the persistent grid
@@ -714,7 +716,6 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   // launch 1: a1 (one CTA); launch 2: the persistent decode grid, programmatically dependent on it
   if (tile) l3_prep_kernel<false, true, true><<<1, kPrepThreads, 0, s>>>(dp.pp);
   else if (wide) l3_prep_kernel<true, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
-  else if (crop && hwc) l3_prep_kernel<false, true, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
   else l3_prep_kernel<false, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -729,8 +730,10 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   if (tile) {
     cfg.blockDim = dim3(kHwcWarps * 32);
     cfg.dynamicSmemBytes = hwc_smem_bytes();
-    return f32 ? cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<true>, dp)
-               : cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<false>, dp);
+    if (crop) return f32 ? cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<true, true>, dp)
+                         : cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<false, true>, dp);
+    return f32 ? cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<true, false>, dp)
+               : cudaLaunchKernelEx(&cfg, l3_decode_hwc_kernel<false, false>, dp);
   }
   cfg.blockDim = dim3(kWarpsPerCta * 32);
   cfg.dynamicSmemBytes = fast_smem_bytes();
@@ -740,8 +743,7 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
     case kU8Wide: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, true, false>, dp);
     case kF32Crop: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<true, false, true>, dp);
     case kU8Crop: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, false, true>, dp);
-    case kF32CropHwc: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<true, false, true, true>, dp);
-    default: return cudaLaunchKernelEx(&cfg, l3_decode_kernel<false, false, true, true>, dp);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -31,6 +31,83 @@ __host__ __device__ constexpr size_t hwc_smem_bytes() {
 constexpr int kStAligned = 0;   // every row start aligned (u8: 4 B, fp32: 16 B): 3 vector stores
 constexpr int kStDynamic = 1;   // rows of varying alignment (image width not a multiple of 4)
 constexpr int kStRagged = 2;    // the patch width is not a multiple of 4: per-column tests
+constexpr int kStWindow = 3;    // crop window (f3): per-pixel validity mask, flip, any alignment
+
+// Crop window of a tile (kStWindow): window row of the tile's current row, window height, which of
+// the lane's 4 output pixels are inside the window and the patch, and the PRMT selector putting the
+// lane's 4 pixels in output order (flip: reversed).
+struct WinRow {
+  int32_t ri;
+  uint32_t chh, cmask, qsel;
+};
+
+// Row of a tile into a crop window, interleaved: the lane's 4 pixels x 3 channels in output order
+// are 12 contiguous elements at optr; whole-lane pixels take the widest store the row's alignment
+// allows (uniform across the warp: lanes differ by 12 / 48 bytes), lanes cut by the window or the
+// patch edge store their valid pixels element by element.
+template <bool F32>
+__device__ __forceinline__ void store12w(uint8_t* optr, const LaneRows& r, const LaneRows& g, const LaneRows& b,
+                                         const float* sc, const float* bi, bool live, const WinRow& wr) {
+  if (!live || (uint32_t)wr.ri >= wr.chh || wr.cmask == 0u) return;
+  const uint32_t qr = prmt(prmt(r.A, r.B, 0x6420u), 0u, wr.qsel);   // [R0 R1 R2 R3] in output order
+  const uint32_t qg = prmt(prmt(g.A, g.B, 0x6420u), 0u, wr.qsel);
+  const uint32_t qb = prmt(prmt(b.A, b.B, 0x6420u), 0u, wr.qsel);
+  if (F32) {
+    float v[12];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      v[3 * t] = fmaf((float)((qr >> (8 * t)) & 0xFFu), sc[0], bi[0]);
+      v[3 * t + 1] = fmaf((float)((qg >> (8 * t)) & 0xFFu), sc[1], bi[1]);
+      v[3 * t + 2] = fmaf((float)((qb >> (8 * t)) & 0xFFu), sc[2], bi[2]);
+    }
+    float* o = reinterpret_cast<float*>(optr);
+    if (wr.cmask == 0xFu) {
+      if ((reinterpret_cast<uintptr_t>(optr) & 15u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+          reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 7u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; q++) reinterpret_cast<float2*>(o)[q] = make_float2(v[2 * q], v[2 * q + 1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 12; e++) o[e] = v[e];
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        if ((wr.cmask >> t) & 1u) {
+          o[3 * t] = v[3 * t];
+          o[3 * t + 1] = v[3 * t + 1];
+          o[3 * t + 2] = v[3 * t + 2];
+        }
+    }
+  } else {
+    const uint32_t x = prmt(qr, qg, 0x5140u);                    // R0 G0 R1 G1
+    const uint32_t y = prmt(qr, qg, 0x7362u);                    // R2 G2 R3 G3
+    const uint32_t w0 = prmt(x, qb, 0x2410u);                    // R0 G0 B0 R1
+    const uint32_t w1 = prmt(prmt(x, qb, 0x0053u), y, 0x5410u);  // G1 B1 R2 G2
+    const uint32_t w2 = prmt(y, qb, 0x7326u);                    // B2 R3 G3 B3
+    const uint32_t wv[3] = {w0, w1, w2};
+    if (wr.cmask == 0xFu) {
+      if ((reinterpret_cast<uintptr_t>(optr) & 3u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) reinterpret_cast<uint32_t*>(optr)[q] = wv[q];
+      } else if ((reinterpret_cast<uintptr_t>(optr) & 1u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; q++)
+          reinterpret_cast<uint16_t*>(optr)[q] = (uint16_t)(wv[q >> 1] >> (16 * (q & 1)));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 12; e++) optr[e] = (uint8_t)(wv[e >> 2] >> (8 * (e & 3)));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 12; e++)
+        if ((wr.cmask >> (e / 3)) & 1u) optr[e] = (uint8_t)(wv[e >> 2] >> (8 * (e & 3)));
+    }
+  }
+}
 
 // Row r of a tile, 4 columns of this lane, interleaved: R0 G0 B0 R1 G1 B1 R2 G2 B2 R3 G3 B3.
 // r/g/b hold the row in pair form (A = columns 0, 1; B = columns 2, 3). kStDynamic picks the widest
@@ -117,8 +194,8 @@ template <bool F32, int MODE, bool STREAM>
 __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint64_t* bars, StreamState* st,
                                               uint32_t* ph, uint32_t h, uint8_t* optr, uint32_t pitch,
                                               const float* sc, const float* bi, uint32_t K, const uint8_t* src,
-                                              uint64_t lim, int lane, uint32_t Lw, bool valid) {
-  constexpr bool FAST = MODE != kStRagged;   // no ghost columns
+                                              uint64_t lim, int lane, uint32_t Lw, bool valid, WinRow wr = {}) {
+  constexpr bool FAST = MODE != kStRagged && MODE != kStWindow;   // window tiles may be ragged: ghost columns
   constexpr bool GUARD = !STREAM;
   constexpr int SLOTS = STREAM ? kHwcSlots : 16;   // whole-staged: one linear 12 KB buffer, no wrap
   constexpr uint32_t rowmax = (12u + 8u * 128u) / 8u + 10u;
@@ -134,8 +211,10 @@ __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint6
   for (int c = 0; c < 3; c++)
     decode_row<true, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, 0, Lw,
                                                               0.f, 0.f, K);
-  store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && s[0].h > 0);
+  if (MODE == kStWindow) store12w<F32>(optr, s[0], s[1], s[2], sc, bi, s[0].h > 0, wr);
+  else store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && s[0].h > 0);
   optr += pitch;
+  wr.ri++;
   for (uint32_t r = 1; r < h; r++) {
     if (STREAM) {
 #pragma unroll
@@ -149,15 +228,40 @@ __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint6
     for (int c = 0; c < 3; c++)
       decode_row<false, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, r,
                                                                  Lw, 0.f, 0.f, K);
-    store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && r < s[0].h);
+    if (MODE == kStWindow) store12w<F32>(optr, s[0], s[1], s[2], sc, bi, r < s[0].h, wr);
+    else store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && r < s[0].h);
     optr += pitch;
+    wr.ri++;
   }
+}
+
+// Output of a tile into the crop window of image d (f3, kStWindow): the lane's lowest-address pixel,
+// the row pitch, and the window row / validity / order of the lane's pixels. Every row of the tile
+// from its top is decoded (the row dependency); rows outside the window store nothing.
+template <bool F32>
+__device__ __forceinline__ uint8_t* hwc_window(const DecodeParams& p, const ImgDesc& d, uint32_t x0, uint32_t y0,
+                                               uint32_t w, uint32_t j4, bool act, WinRow& wr, uint32_t& pitch) {
+  const uint32_t esz = F32 ? 4u : 1u;
+  const bool flip = (d.flip & 1u) != 0;
+  const int32_t cw = (int32_t)d.cw, cj0 = (int32_t)(x0 + j4) - (int32_t)d.cx;
+  const int32_t bc = flip ? cw - 4 - cj0 : cj0;   // window column of the lane's lowest-address pixel
+  wr.ri = (int32_t)y0 - (int32_t)d.cy;
+  wr.chh = d.ch;
+  wr.qsel = flip ? 0x0123u : 0x3210u;
+  wr.cmask = 0;
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int32_t c = flip ? 3 - t : t;
+    if (act && j4 + (uint32_t)c < w && cj0 + c >= 0 && cj0 + c < cw) wr.cmask |= 1u << t;
+  }
+  pitch = (uint32_t)cw * 3u * esz;
+  return reinterpret_cast<uint8_t*>(p.out) + (int64_t)d.out_off * esz + ((int64_t)wr.ri * cw + bc) * 3 * (int64_t)esz;
 }
 
 // N <= 32 (mode 6): G = 32 / L tiles per task, one L-lane segment each (as mode 0 of the planar
 // kernel). The task's 3G units are staged whole into the warp's 12 KB buffer with one barrier;
 // if they do not fit (near-incompressible content), the tiles are staged and decoded one per pass.
-template <bool F32>
+template <bool F32, bool WIN>
 __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const ImgDesc& d, int img, uint32_t t,
                                                    uint8_t* buf, uint64_t* bars, uint32_t ph0, uint64_t lim,
                                                    uint32_t K, int lane) {
@@ -165,14 +269,17 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
   const uint32_t esz = F32 ? 4u : 1u;
   const uint32_t L = d.L, G = d.G;
   const uint32_t seg = (uint32_t)lane / L, j = (uint32_t)lane % L;
-  const uint32_t tile = t * G + seg;
-  const bool tact = tile < d.P;
+  constexpr bool crop = WIN;        // f3 crop window (the kernel instantiation with windows)
+  const uint32_t v = t * G + seg;   // tile of the task's image (crop: among the window's tiles)
+  const bool tact = v < (crop ? d.gxw * d.gyw : d.P);
+  const uint32_t tile = crop ? (d.py0 + v / d.gxw) * d.gx + d.px0 + v % d.gxw : v;
   uint32_t x0 = 0, y0 = 0, w = 0, h = 0;
   if (tact) {
     x0 = (tile % d.gx) * d.N;
     y0 = (tile / d.gx) * d.N;
     w = min(d.N, d.W - x0);
     h = min(d.N, d.H - y0);
+    if (crop) h = min(h, d.cy + d.ch - y0);   // rows below the window are not needed
   }
   const uint32_t nunits = 3u * d.P;
   const uint8_t* file = p.pp.src + d.file_off;
@@ -276,7 +383,14 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
                                                           (pitch & (F32 ? 15u : 3u)) == 0));
     const bool valid = s[0].valid && s[1].h > 0 && s[2].h > 0;
     StreamState* nost = nullptr;
-    if (hmax > 0) {
+    if constexpr (crop) {   // f3: crop window (any alignment, flip, partial lanes)
+      WinRow wr;
+      uint32_t wpitch;
+      uint8_t* wptr = hwc_window<F32>(p, d, x0, y0, w, 4u * j, mine && act[0] && act[1] && act[2], wr, wpitch);
+      if (hmax > 0)
+        hwc_tile_rows<F32, kStWindow, false>(s, buf, bars, nost, nullptr, hmax, wptr, wpitch, sc, bi, K, p.pp.src,
+                                             lim, lane, L, valid, wr);
+    } else if (hmax > 0) {
       if (ragged)
         hwc_tile_rows<F32, kStRagged, false>(s, buf, bars, nost, nullptr, hmax, optr, pitch, sc, bi, K, p.pp.src,
                                              lim, lane, L, valid);
@@ -301,7 +415,8 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
   return ph0;
 }
 
-template <bool F32>
+// WIN: crop windows (f3); a separate instantiation, so the full-image kernel's registers are untouched.
+template <bool F32, bool WIN>
 __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned int ticket;
@@ -339,14 +454,17 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     uint64_t next = 0;
     if (lane == 0) next = grid_warps + atomicAdd(&head->next_task[0], 1ull);
     if (d.mode == 6) {   // N <= 32: G tiles per task, whole-staged
-      ph[0] = hwc_small_task<F32>(p, d, img, pp, rings, bars, ph[0], lim, K, lane);
+      ph[0] = hwc_small_task<F32, WIN>(p, d, img, pp, rings, bars, ph[0], lim, K, lane);
       task = __shfl_sync(0xffffffffu, next, 0);
       continue;
     }
 
-    const uint32_t px = pp % d.gx, py = pp / d.gx;
+    constexpr bool crop = WIN;   // f3: pp counts the window's tiles
+    const uint32_t px = crop ? d.px0 + pp % d.gxw : pp % d.gx, py = crop ? d.py0 + pp / d.gxw : pp / d.gx;
+    const uint32_t tile = py * d.gx + px;
     const uint32_t x0 = px * d.N, y0 = py * d.N;
-    const uint32_t w = min(d.N, d.W - x0), h = min(d.N, d.H - y0);
+    const uint32_t w = min(d.N, d.W - x0);
+    const uint32_t h = crop ? min(min(d.N, d.H - y0), d.cy + d.ch - y0) : min(d.N, d.H - y0);
     const uint32_t nunits = 3u * d.P;
     const uint8_t* file = p.pp.src + d.file_off;
     const uint32_t worst = worst_patch_bytes(w, h);
@@ -357,7 +475,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     bool act[3];
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-      const uint32_t u = (uint32_t)c * d.P + pp;
+      const uint32_t u = (uint32_t)c * d.P + tile;
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
       act[c] = !(unit_offsets_bad(u, nunits, off, nxt, d.data_len));
@@ -399,7 +517,13 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     const float sc[3] = {F32 ? p.scale[0] : 0.f, F32 ? p.scale[1] : 0.f, F32 ? p.scale[2] : 0.f};
     const float bi[3] = {F32 ? p.bias[0] : 0.f, F32 ? p.bias[1] : 0.f, F32 ? p.bias[2] : 0.f};
     const bool valid = s[0].valid;
-    if (ragged)
+    if constexpr (crop) {   // f3: crop window (any alignment, flip, partial lanes)
+      WinRow wr;
+      uint32_t wpitch;
+      uint8_t* wptr = hwc_window<F32>(p, d, x0, y0, w, 4u * lane, act[0] && act[1] && act[2], wr, wpitch);
+      hwc_tile_rows<F32, kStWindow, true>(s, rings, bars, st, ph, h, wptr, wpitch, sc, bi, K, p.pp.src, lim, lane,
+                                          32u, valid, wr);
+    } else if (ragged)
       hwc_tile_rows<F32, kStRagged, true>(s, rings, bars, st, ph, h, optr, pitch, sc, bi, K, p.pp.src, lim, lane,
                                           32u, valid);
     else if (aligned_all)
@@ -414,7 +538,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
       const bool err = act[c] && (s[c].kacc >= 0x80000000u || s[c].bp > s[c].lim);
       if (err && lane == 0) {   // a7: exact first error of a failed unit
         const int code = unit_first_error(p.pp.src, start[c], end[c], w, h);
-        if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + pp, code));
+        if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
       }
       while (st[c].landed < st[c].issued) {   // drain copies that were issued but never waited for
         const uint32_t sl = st[c].landed % kHwcSlots;
