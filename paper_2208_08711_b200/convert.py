@@ -86,10 +86,14 @@ def convert(paths: Sequence[str], out_dir: str | None = None, batch: int = 64, p
         os.makedirs(out_dir, exist_ok=True)
     raw = comp = 0
     ratios = []
+    enc_ms = 0.0
     for b0 in range(0, len(files), batch):
         chunk = files[b0:b0 + batch]
         imgs = [load_planar(p) for p in chunk]
-        src, offs = encode_batch(imgs, patch_sizes=[patch] * len(imgs), device=device, predictor=predictor)
+        timing = {}
+        src, offs = encode_batch(imgs, patch_sizes=[patch] * len(imgs), device=device, predictor=predictor,
+                                 timing=timing)
+        enc_ms += timing["encode_ms"]
         o = offs.cpu().numpy()
         buf = src.cpu().numpy() if int(o[-1]) else np.zeros(0, np.uint8)
         for p, im, a, b in zip(chunk, imgs, o[:-1], o[1:]):
@@ -111,6 +115,9 @@ def convert(paths: Sequence[str], out_dir: str | None = None, batch: int = 64, p
         "ratio_max": round(max(ratios), 4) if ratios else None,
         "format": "L3IP (original Paeth)" if predictor else "L3IF",
         "patch": patch or "policy (PAPER.md:166)",
+        # the GPU encoder alone (l3_encode_batch device time, images already in HBM): raw input bytes / s
+        "encode_ms": round(enc_ms, 3),
+        "encoder_raw_gbs": round(raw / (enc_ms / 1e3) / 1e9, 2) if enc_ms > 0 else None,
     }
 
 

@@ -4,8 +4,9 @@
 // encoder under the same readings (C1 residual mod 256, C2 signed
 // base for residual rows, C3 tie order, C4 clamp-to-edge, C5 first row per
 // patch, C6 k >= 1, C8 MSB-first rows, byte-aligned patches, C9 container).
-// Not on the decode hot path; kept simple: one warp per (image, channel, patch)
-// unit, 1 column per lane per step.
+// Not on the decode hot path: one warp per (image, channel, patch) unit, 4
+// consecutive columns per lane; each lane ORs its 4 deltas into the unit's
+// shared-memory bitstream as one field (two word atomics per lane and row).
 //
 //   E1 l3_enc_size_kernel   bytes of every unit (two-pass: sizes first)
 //   E2 l3_enc_scan_kernel   per image: unit offsets (exclusive scan) + file size
@@ -99,21 +100,48 @@ __device__ __forceinline__ int residual(const UnitGeom& g, uint32_t r, uint32_t 
   return (x - paeth_pred(tl, t, tr)) & 0xFF;
 }
 
-// Row base-delta parameters (readings C2/C6); warp-collective.
-__device__ __forceinline__ void row_kb(const UnitGeom& g, uint32_t r, int lane, int predictor, int* k,
-                                       int* base) {
+// Columns per lane: 4 consecutive columns for wide patches, fewer for narrow ones so that all 32
+// lanes stay busy (N = 32: one column per lane).
+__device__ __forceinline__ uint32_t enc_cpl(uint32_t w) { return w > 64u ? 4u : (w > 32u ? 2u : 1u); }
+
+// The residuals of cpl (<= 4) consecutive columns c0 .. of row r (byte i = column c0+i; columns past
+// the patch width are 0) and how many of them are real.
+__device__ __forceinline__ uint32_t residual4(const UnitGeom& g, uint32_t r, uint32_t c0, uint32_t cpl, int predictor,
+                                              uint32_t* nvalid) {
+  const uint32_t nv = c0 < g.w ? min(cpl, g.w - c0) : 0u;
+  uint32_t q = 0;
+  for (uint32_t i = 0; i < nv; i++) q |= (uint32_t)residual(g, r, c0 + i, predictor) << (8 * i);
+  *nvalid = nv;
+  return q;
+}
+
+// Row base-delta parameters (readings C2/C6) over the residual words of the row, one
+// word (4 columns) per lane and 128-column chunk; warp-collective. Rows >= 1 compare residuals as
+// signed bytes (reading C2), row 0 (raw pixels) unsigned.
+constexpr int kEncChunks = 2;   // 4 columns x 32 lanes x 2 = 256 >= every N (u8 header field)
+__device__ __forceinline__ void row_kb4(const uint32_t* q, const uint32_t* nv, uint32_t r, int* k, int* base) {
   int mn = 1 << 20, mx = -(1 << 20);
-  for (uint32_t c = lane; c < g.w; c += 32) {
-    int v = residual(g, r, c, predictor);
-    if (r > 0 && v >= 128) v -= 256;
-    mn = min(mn, v);
-    mx = max(mx, v);
-  }
+#pragma unroll
+  for (int m = 0; m < kEncChunks; m++)
+    for (uint32_t i = 0; i < nv[m]; i++) {
+      int v = (int)((q[m] >> (8 * i)) & 0xFFu);
+      if (r > 0 && v >= 128) v -= 256;
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
   mn = __reduce_min_sync(0xffffffffu, mn);
   mx = __reduce_max_sync(0xffffffffu, mx);
   const int span = mx - mn;
   *k = span > 0 ? 32 - __clz(span) : 1;
   *base = mn & 0xFF;
+}
+
+// All residual words of row r for this lane: column chunk m covers columns 32 cpl m + cpl lane ...
+__device__ __forceinline__ void row_words(const UnitGeom& g, uint32_t r, int lane, int predictor, uint32_t* q,
+                                          uint32_t* nv) {
+  const uint32_t cpl = enc_cpl(g.w);
+#pragma unroll
+  for (int m = 0; m < kEncChunks; m++) q[m] = residual4(g, r, 32u * cpl * m + cpl * lane, cpl, predictor, &nv[m]);
 }
 
 __global__ void l3_enc_size_kernel(EncParams p) {
@@ -125,8 +153,10 @@ __global__ void l3_enc_size_kernel(EncParams p) {
     const UnitGeom g = unit_geom(p, d, (uint32_t)(u - d.unit0));
     uint64_t bits = 0;
     for (uint32_t r = 0; r < g.h; r++) {
+      uint32_t q[kEncChunks], nv[kEncChunks];
+      row_words(g, r, lane, p.predictor, q, nv);
       int k, base;
-      row_kb(g, r, lane, p.predictor, &k, &base);
+      row_kb4(q, nv, r, &k, &base);
       bits += 12u + (uint64_t)k * g.w;
     }
     if (lane == 0) p.ws.unit_bytes[u] = (uint32_t)((bits + 7) / 8);
@@ -182,17 +212,14 @@ __global__ void l3_enc_files_kernel(EncParams p) {
   }
 }
 
-__device__ __forceinline__ void or_byte(uint32_t* words, uint32_t byte, uint32_t v) {
-  if (v) atomicOr(&words[byte >> 2], v << ((byte & 3) * 8));
-}
-
-// Put `nbits` (<= 12) of `v` at bit position `pos` (MSB-first) into a zeroed byte buffer.
-__device__ __forceinline__ void put_bits(uint32_t* words, uint32_t pos, uint32_t v, uint32_t nbits) {
-  const uint32_t b0 = pos >> 3, sh = pos & 7;
-  const uint32_t win = v << (24 - sh - nbits);   // 24-bit big-endian window
-  or_byte(words, b0, (win >> 16) & 0xFF);
-  or_byte(words, b0 + 1, (win >> 8) & 0xFF);
-  or_byte(words, b0 + 2, win & 0xFF);
+// OR the `nbits` (<= 32) MSB-aligned bits of F into the stream at bit position `pos` (reading C8,
+// MSB-first): stream words are big-endian in `words` (bit 31 = first bit), so a field touches at
+// most two words — two shared-memory atomics per lane and row instead of one per byte and delta.
+__device__ __forceinline__ void put_field(uint32_t* words, uint32_t pos, uint32_t F, uint32_t nbits) {
+  if (nbits == 0) return;
+  const uint32_t w0 = pos >> 5, sh = pos & 31u;
+  atomicOr(&words[w0], F >> sh);
+  if (sh + nbits > 32u) atomicOr(&words[w0 + 1], F << (32u - sh));
 }
 
 __global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
@@ -216,24 +243,31 @@ __global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
       else b = (uint8_t)d.N;
       file[lane] = b;
     }
-    const uint32_t words = (nbytes + 3) / 4;
+    const uint32_t words = (nbytes + 3) / 4 + 1;
     for (uint32_t x = lane; x < words && x < smem_words; x += 32) buf[x] = 0;
     __syncwarp();
     uint32_t pos = 0;
     for (uint32_t r = 0; r < g.h; r++) {
+      uint32_t q[kEncChunks], nv[kEncChunks];
+      row_words(g, r, lane, p.predictor, q, nv);
       int k, base;
-      row_kb(g, r, lane, p.predictor, &k, &base);
-      if (lane == 0) put_bits(buf, pos, ((uint32_t)k << 8) | (uint32_t)base, 12);
-      for (uint32_t c = lane; c < g.w; c += 32) {
-        const uint32_t delta = (uint32_t)(residual(g, r, c, p.predictor) - base) & 0xFFu;
-        put_bits(buf, pos + 12u + c * (uint32_t)k, delta, (uint32_t)k);
+      row_kb4(q, nv, r, &k, &base);
+      if (lane == 0) put_field(buf, pos, (((uint32_t)k << 8) | (uint32_t)base) << 20, 12);
+      // a4 in reverse: the lane's deltas (residual - base) mod 256 as one MSB-first k-bit field each
+#pragma unroll
+      for (int m = 0; m < kEncChunks; m++) {
+        uint32_t F = 0;
+        for (uint32_t t = 0; t < nv[m]; t++) F = (F << k) | ((((q[m] >> (8 * t)) & 0xFFu) - (uint32_t)base) & 0xFFu);
+        const uint32_t nb = nv[m] * (uint32_t)k;
+        const uint32_t cpl = enc_cpl(g.w);
+        if (nb) put_field(buf, pos + 12u + (32u * cpl * m + cpl * (uint32_t)lane) * (uint32_t)k, F << (32u - nb), nb);
       }
       pos += 12u + (uint32_t)k * g.w;
     }
     __syncwarp();
+    // big-endian stream words -> bytes
     uint8_t* out = file + d.hdr + off;
-    const uint8_t* b8 = reinterpret_cast<const uint8_t*>(buf);
-    for (uint32_t x = lane; x < nbytes; x += 32) out[x] = b8[x];
+    for (uint32_t x = lane; x < nbytes; x += 32) out[x] = (uint8_t)(buf[x >> 2] >> (24 - 8 * (x & 3)));
     __syncwarp();
   }
 }
@@ -323,7 +357,7 @@ l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s) {
   l3_enc_size_kernel<<<grid1, 256, 0, s>>>(p);
   l3_enc_scan_kernel<<<a->n, 1024, 0, s>>>(p);
   l3_enc_files_kernel<<<1, 32, 0, s>>>(p);
-  const uint32_t smem_words = (pl.worst_patch + 16) / 4 + 1;
+  const uint32_t smem_words = (pl.worst_patch + 16) / 4 + 2;
   const size_t smem = (size_t)smem_words * 4;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(l3_enc_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
