@@ -72,7 +72,7 @@ def launches_md(path):
     for k in order:
         v = agg[k]
         out.append(f"| `{k[:90]}` | {len(v)} | {sum(v) / len(v):.2f} |")
-    step = [k for k in order if ("parse" in k or "decode" in k) and len(agg[k]) >= 5]
+    step = [k for k in order if ("parse" in k or "decode" in k or "prep" in k) and len(agg[k]) >= 5]
     per = {k: sum(agg[k][-5:]) / len(agg[k][-5:]) for k in step}
     tot = sum(per.values())
     out.append("\nShare of one decode step (mean of the last launches of each step kernel): " + ", ".join(
