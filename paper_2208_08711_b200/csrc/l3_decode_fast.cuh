@@ -193,6 +193,9 @@ __device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_
   return prmt(X, tr, sel);                   // pair form: bytes 1 and 3 are zero
 }
 
+#ifndef L3_U8_V16
+#define L3_U8_V16 0   // A/B: u8 rows as 128-bit stores (4-lane shuffle gather) where aligned; measured slower
+#endif
 #ifndef L3_MIN_CTAS
 #define L3_MIN_CTAS 6   // __launch_bounds__ min CTAs per SM for the planar kernels: register cap 80, no spills
 #endif
@@ -256,6 +259,7 @@ struct LaneRows {
   uint32_t selL;      // PRMT selector (left lane's Q, Q) -> [c-1 c0 c1 c2], clamped at column 0
   uint32_t selR;      // PRMT selector (Q, right lane's Q) -> [c1 c2 c3 c4], clamped at the last lane
   uint32_t selG;      // RAGGED: PRMT selector replicating column w-1 into the lane's ghost columns
+  bool v16;           // u8 FAST: 16-byte rows (every 4 lanes' words gathered into one 128-bit store)
   // CROP variant only (f3, partial decode): output window mapping
   int32_t ri;         // current image row - crop top
   uint32_t chh;       // crop height
@@ -300,7 +304,7 @@ __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t 
 
 // Byte-form variant of store4: q = [c0 c1 c2 c3].
 template <bool F32, bool FAST, bool RAGGED = !FAST>
-__device__ __forceinline__ void store4q(const LaneRows& s, uint32_t q, float sc, float bi, bool pred) {
+__device__ __forceinline__ void store4q(const LaneRows& s, uint32_t q, float sc, float bi, bool pred, uint32_t Lw) {
   if (F32) {
     const float v0 = fmaf((float)(q & 0xFFu), sc, bi), v1 = fmaf((float)((q >> 8) & 0xFFu), sc, bi);
     const float v2 = fmaf((float)((q >> 16) & 0xFFu), sc, bi), v3 = fmaf((float)(q >> 24), sc, bi);
@@ -317,7 +321,15 @@ __device__ __forceinline__ void store4q(const LaneRows& s, uint32_t q, float sc,
       if (!RAGGED || s.j4 + 3 < s.w) o[3] = v3;
     }
   } else {
-    if (FAST) {
+    if (FAST && s.v16) {   // 128-bit stores: lane 4m gathers lanes 4m+1..4m+3's words (warp-uniform branch)
+      const uint32_t q1 = __shfl_down_sync(0xffffffffu, q, 1, Lw);
+      const uint32_t q2 = __shfl_down_sync(0xffffffffu, q, 2, Lw);
+      const uint32_t q3 = __shfl_down_sync(0xffffffffu, q, 3, Lw);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+          "@p st.global.v4.b32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(s.optr),
+          "r"(q), "r"(q1), "r"(q2), "r"(q3), "r"((uint32_t)(pred && (s.j4 & 15u) == 0)));
+    } else if (FAST) {
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
           "@p st.global.b32 [%0], %1;\n\t}" ::"l"(s.optr), "r"(q), "r"((uint32_t)pred));
@@ -403,7 +415,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     uint32_t q = prmt(xA, xB, 0x6420u);   // [c0 c1 c2 c3] mod 256
     if (RAGGED) q = prmt(q, 0u, s.selG);  // columns >= w: ghosts of column w-1
     if (CROP) store4_crop<F32, HWC, true>(s, q, 0u, sc, bi, live);
-    else store4q<F32, FAST, RAGGED>(s, q, sc, bi, live && s.valid);
+    else store4q<F32, FAST, RAGGED>(s, q, sc, bi, live && s.valid, Lw);
     s.Q = q;
   } else {
   if (FIRST) {
@@ -725,6 +737,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_M
                                                                    (F32 ? 15 : 3)) == 0) &&
                                                                  ((s.pitch & (F32 ? 15u : 3u)) == 0))));
     const bool fast = __all_sync(0xffffffffu, fast_ok);
+    // u8: whole 16-byte lane groups (patch width a multiple of 16, 16-byte aligned rows) store 128 bits
+    s.v16 = !F32 && !CROP && L3_U8_V16 != 0 &&
+            __all_sync(0xffffffffu, !active || ((w & 15u) == 0 && ((reinterpret_cast<uintptr_t>(s.optr) - s.j4) & 15u) == 0 &&
+                                                (s.pitch & 15u) == 0));
     // u8 narrow variant, whole-staged N <= 32 tasks (small mixed-shape images, e.g. C2): planar
     // output that is not vector-aligned (image width not a multiple of 4) but has no ragged patch
     // takes scalar stores without per-column tests or edge ghosts. Everything else keeps two paths

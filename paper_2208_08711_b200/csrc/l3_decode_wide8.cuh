@@ -96,6 +96,7 @@ __device__ __forceinline__ void w8_advance(const uint8_t* src, uint64_t lim, Seg
 struct Lane8 {
   uint32_t bp, lim, w, h, j8, raw, kacc;
   bool first, last, valid;
+  bool v16;   // u8 FAST: 128-bit stores (lane 2m gathers lane 2m+1's 8 bytes), rows 16-byte aligned
   uint8_t* optr;
   uint32_t pitch;
   uint32_t A, B, C, D;
@@ -114,7 +115,7 @@ __device__ __forceinline__ void unpack4(uint32_t f, uint32_t sh, uint32_t pk, ui
 
 template <bool F32, bool FAST>
 __device__ __forceinline__ void store8(const Lane8& s, uint32_t xA, uint32_t xB, uint32_t xC, uint32_t xD, float sc,
-                                       float bi, bool pred) {
+                                       float bi, bool pred, uint32_t L) {
   if (F32) {
     const float v0 = fmaf((float)(xA & 0xFFFFu), sc, bi), v1 = fmaf((float)(xA >> 16), sc, bi);
     const float v2 = fmaf((float)(xB & 0xFFFFu), sc, bi), v3 = fmaf((float)(xB >> 16), sc, bi);
@@ -135,7 +136,13 @@ __device__ __forceinline__ void store8(const Lane8& s, uint32_t xA, uint32_t xB,
     }
   } else {
     const uint32_t q0 = prmt(xA, xB, 0x6420), q1 = prmt(xC, xD, 0x6420);
-    if (FAST) {
+    if (FAST && s.v16) {   // warp-uniform: 128-bit stores by the even lanes
+      const uint32_t r0 = __shfl_down_sync(0xffffffffu, q0, 1, L), r1 = __shfl_down_sync(0xffffffffu, q1, 1, L);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+          "@p st.global.v4.b32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(s.optr), "r"(q0), "r"(q1), "r"(r0), "r"(r1),
+          "r"((uint32_t)(pred && (s.j8 & 15u) == 0)));
+    } else if (FAST) {
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
           "@p st.global.v2.b32 [%0], {%1, %2};\n\t}" ::"l"(s.optr), "r"(q0), "r"(q1), "r"((uint32_t)pred));
@@ -261,7 +268,7 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
     xC = x[4] | (x[5] << 16);
     xD = x[6] | (x[7] << 16);
   }
-  store8<F32, FAST>(s, xA, xB, xC, xD, sc, bi, live && s.valid);
+  store8<F32, FAST>(s, xA, xB, xC, xD, sc, bi, live && s.valid, L);
   s.A = xA;
   s.B = xB;
   s.C = xC;
@@ -379,6 +386,9 @@ __device__ __forceinline__ uint32_t decode_task8(const DecodeParams& p, const Im
   const bool fast_ok = !active || ((w & 7u) == 0 && ((reinterpret_cast<uintptr_t>(s.optr) & align) == 0) &&
                                    ((s.pitch & align) == 0));
   const bool fast = __all_sync(0xffffffffu, fast_ok);
+  s.v16 = !F32 && L3_U8_V16 != 0 &&
+          __all_sync(0xffffffffu, !active || ((w & 15u) == 0 && ((reinterpret_cast<uintptr_t>(s.optr) - s.j8) & 15u) == 0 &&
+                                              (s.pitch & 15u) == 0));
   const bool guard = hmin != hmax;    // segments of unequal height (or an idle segment)
   const float sc = F32 ? (ch == 0 ? p.scale[0] : (ch == 1 ? p.scale[1] : p.scale[2])) : 0.f;
   const float bi = F32 ? (ch == 0 ? p.bias[0] : (ch == 1 ? p.bias[1] : p.bias[2])) : 0.f;
