@@ -222,10 +222,33 @@ __device__ __forceinline__ void put_field(uint32_t* words, uint32_t pos, uint32_
   if (sh + nbits > 32u) atomicOr(&words[w0 + 1], F << (32u - sh));
 }
 
-__global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
-  extern __shared__ uint32_t buf[];
-  const int lane = threadIdx.x & 31;
-  for (uint64_t u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+// E4: one warp per unit, rows in order. The unit's bitstream is written straight to the file with
+// aligned 32-bit stores: bit b of the stream lives in the aligned word holding byte a + b/8, where a =
+// the unit's start address mod 4. Each row's fields are ORed into a small per-warp window of words
+// in shared memory (two word atomics per lane); after the row, the completed words go to global
+// memory and the partial last word moves to the window's front. Words the unit shares with its
+// neighbours (its first and last) are written byte by byte. No patch-sized buffer: 8 warps per block.
+constexpr int kEncPackWarps = 8;
+constexpr uint32_t kEncWin = 80;   // words: the carried word + one row (12 + 8 x 255 bits = 65 words)
+
+__device__ __forceinline__ void enc_store_word(uint8_t* base, uint32_t w, uint32_t word, uint32_t a, uint32_t nbytes) {
+  // stream bytes [a, a + nbytes) of the aligned region at base; word w covers bytes [4w, 4w + 4)
+  const uint32_t lo = 4u * w, hi = lo + 4u;
+  if (lo >= a && hi <= a + nbytes) {
+    *reinterpret_cast<uint32_t*>(base + lo) = bswap32(word);
+  } else {
+#pragma unroll
+    for (uint32_t i = 0; i < 4; i++)
+      if (lo + i >= a && lo + i < a + nbytes) base[lo + i] = (uint8_t)(word >> (24 - 8 * i));
+  }
+}
+
+__global__ void __launch_bounds__(kEncPackWarps * 32) l3_enc_pack_kernel(EncParams p) {
+  __shared__ uint32_t win_all[kEncPackWarps][kEncWin];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* win = win_all[warp];
+  const uint64_t warps = (uint64_t)gridDim.x * kEncPackWarps;
+  for (uint64_t u = (uint64_t)blockIdx.x * kEncPackWarps + warp; u < p.total_units; u += warps) {
     const int i = find_image(p.ws.unit_prefix, p.n, u);
     const EncDesc d = p.ws.desc[i];
     const uint32_t ul = (uint32_t)(u - d.unit0);
@@ -243,31 +266,44 @@ __global__ void l3_enc_pack_kernel(EncParams p, uint32_t smem_words) {
       else b = (uint8_t)d.N;
       file[lane] = b;
     }
-    const uint32_t words = (nbytes + 3) / 4 + 1;
-    for (uint32_t x = lane; x < words && x < smem_words; x += 32) buf[x] = 0;
+    uint8_t* dst = file + d.hdr + off;
+    const uint32_t a = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 3u);
+    uint8_t* base = dst - a;                   // aligned start of the unit's words
+    const uint32_t span = min(kEncWin, (31u + 12u + 8u * g.w) / 32u + 2u);   // window words one row can touch
+    for (uint32_t x = lane; x < span; x += 32) win[x] = 0;
     __syncwarp();
-    uint32_t pos = 0;
+    uint32_t wbase = 0;                        // stream word index of win[0]
+    uint32_t pos = 8u * a;                     // bit position of the current row in the aligned stream
     for (uint32_t r = 0; r < g.h; r++) {
       uint32_t q[kEncChunks], nv[kEncChunks];
       row_words(g, r, lane, p.predictor, q, nv);
-      int k, base;
-      row_kb4(q, nv, r, &k, &base);
-      if (lane == 0) put_field(buf, pos, (((uint32_t)k << 8) | (uint32_t)base) << 20, 12);
+      int k, base8;
+      row_kb4(q, nv, r, &k, &base8);
+      const uint32_t wp = pos - 32u * wbase;   // row position inside the window
+      if (lane == 0) put_field(win, wp, (((uint32_t)k << 8) | (uint32_t)base8) << 20, 12);
       // a4 in reverse: the lane's deltas (residual - base) mod 256 as one MSB-first k-bit field each
+      const uint32_t cpl = enc_cpl(g.w);
 #pragma unroll
       for (int m = 0; m < kEncChunks; m++) {
         uint32_t F = 0;
-        for (uint32_t t = 0; t < nv[m]; t++) F = (F << k) | ((((q[m] >> (8 * t)) & 0xFFu) - (uint32_t)base) & 0xFFu);
+        for (uint32_t t = 0; t < nv[m]; t++) F = (F << k) | ((((q[m] >> (8 * t)) & 0xFFu) - (uint32_t)base8) & 0xFFu);
         const uint32_t nb = nv[m] * (uint32_t)k;
-        const uint32_t cpl = enc_cpl(g.w);
-        if (nb) put_field(buf, pos + 12u + (32u * cpl * m + cpl * (uint32_t)lane) * (uint32_t)k, F << (32u - nb), nb);
+        if (nb) put_field(win, wp + 12u + (32u * cpl * m + cpl * (uint32_t)lane) * (uint32_t)k, F << (32u - nb), nb);
       }
       pos += 12u + (uint32_t)k * g.w;
+      __syncwarp();
+      // flush the completed words, carry the partial one to the window front
+      const uint32_t done = (pos >> 5) - wbase;   // complete words in the window
+      for (uint32_t x = lane; x < done; x += 32) enc_store_word(base, wbase + x, win[x], a, nbytes);
+      __syncwarp();
+      const uint32_t carry = win[done];
+      __syncwarp();
+      for (uint32_t x = lane; x < span; x += 32) win[x] = (x == 0) ? carry : 0u;
+      wbase += done;
+      __syncwarp();
     }
-    __syncwarp();
-    // big-endian stream words -> bytes
-    uint8_t* out = file + d.hdr + off;
-    for (uint32_t x = lane; x < nbytes; x += 32) out[x] = (uint8_t)(buf[x >> 2] >> (24 - 8 * (x & 3)));
+    // the last (partial) word: the stream is padded to whole bytes (nbytes), the rest belongs to the next unit
+    if (lane == 0 && 32u * wbase < 8u * (a + nbytes)) enc_store_word(base, wbase, win[0], a, nbytes);
     __syncwarp();
   }
 }
@@ -357,14 +393,9 @@ l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s) {
   l3_enc_size_kernel<<<grid1, 256, 0, s>>>(p);
   l3_enc_scan_kernel<<<a->n, 1024, 0, s>>>(p);
   l3_enc_files_kernel<<<1, 32, 0, s>>>(p);
-  const uint32_t smem_words = (pl.worst_patch + 16) / 4 + 2;
-  const size_t smem = (size_t)smem_words * 4;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(l3_enc_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-    return L3_E_CUDA;
-  const int grid4 = (int)(pl.units < (uint64_t)sms * 32 ? pl.units : (uint64_t)sms * 32);
-  l3_enc_pack_kernel<<<grid4, 32, smem, s>>>(p, smem_words);
+  const uint64_t want4 = (pl.units + kEncPackWarps - 1) / kEncPackWarps;
+  const int grid4 = (int)(want4 < (uint64_t)sms * 8 ? want4 : (uint64_t)sms * 8);
+  l3_enc_pack_kernel<<<grid4, kEncPackWarps * 32, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
