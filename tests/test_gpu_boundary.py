@@ -330,3 +330,45 @@ def test_bench_two_ranks_share_device():
     roof = d["roofline"]
     assert 0 < roof["aggregate_frac"] and roof["aggregate_alg_bytes"] > roof["alg_bytes_per_launch"]
     assert d["e2e"]["value"] > 0 and d["value"] > 0
+
+
+def test_decode_in_cuda_graph():
+    """l3_decode_batch captured in a CUDA graph (its two launches and their programmatic dependency
+    become graph nodes) and replayed on new inputs copied into the captured buffers: pixels and
+    statuses equal the oracle's on every replay."""
+    imgs = [l3synth.natural(200, 300, 30 + i, 2.0) for i in range(4)]
+    files = [l3ref.encode(im) for im in imgs]
+    other = [l3synth.natural(200, 300, 40 + i, 2.0) for i in range(4)]
+    files2 = [l3ref.encode(im) for im in other]
+    cap = max(sum(map(len, files)), sum(map(len, files2))) + 16
+    src = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+    offs = torch.zeros(5, dtype=torch.int64, device="cuda")
+    shapes = torch.tensor([[200, 300]] * 4, dtype=torch.int32, device="cuda")
+    out = torch.zeros((4, 3, 200, 300), dtype=torch.uint8, device="cuda")
+    dec = BatchDecoder(4)
+    s = torch.cuda.Stream()
+
+    def load(fs):
+        o = np.cumsum([0] + [len(f) for f in fs])
+        src[:int(o[-1])].copy_(torch.from_numpy(np.frombuffer(b"".join(fs), np.uint8).copy()))
+        offs.copy_(torch.from_numpy(o.astype(np.int64)))
+
+    load(files)
+    torch.cuda.synchronize()
+    a = dec.args(src, offs, shapes, out)
+    with torch.cuda.stream(s):
+        l3.l3_decode_batch(a, s)   # warm up outside the capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        l3.l3_decode_batch(a, s)
+    for fs, ref in ((files, imgs), (files2, other), (files, imgs)):
+        load(fs)
+        out.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert dec.status[:4].cpu().tolist() == [0] * 4
+        got = out.cpu().numpy()
+        for i in range(4):
+            assert np.array_equal(got[i], ref[i]), i
