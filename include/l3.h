@@ -186,6 +186,14 @@ l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream);
  * Returns INVALID_ARGUMENT for a NULL out, CUDA on a launch error; async. */
 l3_status_t l3_selftest_paeth4(uint8_t* out, l3_stream_t stream);
 
+/* Exhaustive self-test of the biased-half (fp16x2) predictor used by the fp32
+ * planar and crop decode paths (same rule, Fig. 3; ties TL, T, TR;
+ * samples held as the fp16 values 1024 + c).
+ * out: device, 2^24 bytes; out[TL<<16 | T<<8 | TR] = predicted byte (0xEE if the
+ * result lost its bias byte). Returns INVALID_ARGUMENT for a NULL out, CUDA on a
+ * launch error; async. */
+l3_status_t l3_selftest_paeth_h2(uint8_t* out, l3_stream_t stream);
+
 /* Human-readable name of a status code; never NULL. */
 const char* l3_status_string(int32_t status);
 

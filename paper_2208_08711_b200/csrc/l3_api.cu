@@ -10,6 +10,7 @@ cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_va
 cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s);
 cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s);
 cudaError_t launch_selftest_paeth4(uint8_t* out, cudaStream_t s);
+cudaError_t launch_selftest_paeth_h2(uint8_t* out, cudaStream_t s);
 cudaError_t launch_ablation(const l3_decode_args* a, int mode, cudaStream_t s);
 uint64_t encode_workspace_size(const int32_t* shapes, const int32_t* n_host, int32_t n);
 l3_status_t encode_batch(const l3_encode_args* a, cudaStream_t s);
@@ -77,6 +78,11 @@ l3_status_t l3_selftest_paeth(uint8_t* out, l3_stream_t stream) {
 l3_status_t l3_selftest_paeth4(uint8_t* out, l3_stream_t stream) {
   if (!out) return L3_E_INVALID_ARGUMENT;
   return l3::launch_selftest_paeth4(out, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
+}
+
+l3_status_t l3_selftest_paeth_h2(uint8_t* out, l3_stream_t stream) {
+  if (!out) return L3_E_INVALID_ARGUMENT;
+  return l3::launch_selftest_paeth_h2(out, (cudaStream_t)stream) == cudaSuccess ? L3_OK : L3_E_CUDA;
 }
 
 const char* l3_status_string(int32_t s) {

@@ -143,7 +143,8 @@ __device__ __forceinline__ int parse_header(const ParseParams& p, int i, ImgDesc
 }
 
 // a1 without the tail zone (kernel variants without the wide path): one pass.
-// HWCK: the HWC kernel's decomposition: one task per (image, patch) for N <= 128 (mode 5).
+// HWCK: the HWC tile kernel's decomposition: one task per (image, patch) for 33 <= N <= 128 (mode 5),
+// G tiles per task for N <= 32 (mode 6).
 template <bool VARIANT = false, bool AUG = false, bool HWCK = false>
 __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b) {
   uint64_t carry0 = 0, carry1 = 0;
@@ -283,7 +284,7 @@ template <bool WIDE, bool AUG, bool HWCK>
 __global__ void __launch_bounds__(kPrepThreads) l3_prep_kernel(ParseParams p) {
   pdl_launch_dependents();
   __shared__ uint64_t sh_a[33], sh_b[33];
-  if (HWCK) parse_phase_simple<false, true, true>(p, sh_a, sh_b);
+  if (HWCK) parse_phase_simple<false, true, HWCK>(p, sh_a, sh_b);
   else parse_phase<WIDE, AUG>(p, sh_a, sh_b);
 }
 
@@ -591,6 +592,30 @@ __global__ void l3_selftest_paeth4_kernel(uint8_t* out) {
 
 cudaError_t launch_selftest_paeth4(uint8_t* out, cudaStream_t s) {
   l3_selftest_paeth4_kernel<<<(1u << 24) / 256, 256, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
+// Exhaustive self-test of the biased-half predictor (paeth_h2): out[TL<<16 | T<<8 | TR] = predicted
+// byte, two triples per thread (one per half); a result whose halves lose the 0x64 bias byte, or where
+// paeth_pred2 on the same biased inputs disagrees in the low bytes, is 0xEE (its bytes 1 and 3 are
+// either the bias or zero; the decode masks them).
+__global__ void l3_selftest_paeth_h2_kernel(uint8_t* out) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) * 2u;
+  if (i >= (1u << 24)) return;
+  const uint32_t a = i, b = i + 1;
+  const uint32_t tl = ((a >> 16) & 0xFFu) | (((b >> 16) & 0xFFu) << 16) | 0x64006400u;
+  const uint32_t t = ((a >> 8) & 0xFFu) | (((b >> 8) & 0xFFu) << 16) | 0x64006400u;
+  const uint32_t tr = (a & 0xFFu) | ((b & 0xFFu) << 16) | 0x64006400u;
+  const uint32_t p2 = paeth_h2(tl, t, tr);
+  out[a] = (uint8_t)(p2 & 0xFFu);
+  out[b] = (uint8_t)((p2 >> 16) & 0xFFu);
+  // the pair-form predictor on biased inputs (mixed lanes, L3_H2_F32) must agree and keep the bias
+  if ((p2 & 0xFF00FF00u) != 0x64006400u || ((paeth_pred2(tl, t, tr, 128u) ^ p2) & 0x00FF00FFu) != 0u)
+    out[a] = out[b] = 0xEE;
+}
+
+cudaError_t launch_selftest_paeth_h2(uint8_t* out, cudaStream_t s) {
+  l3_selftest_paeth_h2_kernel<<<(1u << 23) / 256, 256, 0, s>>>(out);
   return cudaGetLastError();
 }
 

@@ -193,11 +193,55 @@ __device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_
   return prmt(X, tr, sel);                   // pair form: bytes 1 and 3 are zero
 }
 
+// Custom Paeth predictor (Fig. 3; ties TL, T, TR — reading C3) for two samples held as
+// BIASED HALVES: each 16-bit half is the fp16 value 1024 + c (bits 0x6400 | c), so differences are exact
+// small integers and the bits stay an integer pair for the mod-256 residual add. With a = TL - T,
+// b = TR - T, s = a + b the distances are d(TL) = |b|, d(T) = |s|, d(TR) = |a|, and for
+// integers sat(x - y) = [x > y]. TL wins iff |b| <= |a| and |b| <= |s|; TR iff |a| < |b| and |a| < |s|;
+// else T. So pred = T + a·[TL wins] + b·[TR wins] = 11 HADD2 / HFMA2 / HMUL2 (|x| and .SAT are operand
+// and result modifiers): the predictor runs on the FMA / FP16 pipes instead of the half-rate ALU pipe.
+// Every intermediate is an integer of magnitude <= 1534 (exact in fp16). DESIGN.md §5;
+// exhaustively checked by l3_selftest_paeth_h2.
+__device__ __forceinline__ __half2 u2h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t tr) {
+  const __half2 TL = u2h2(tl), T = u2h2(t), TR = u2h2(tr);
+  const __half2 a = __hsub2(TL, T), b = __hsub2(TR, T), s = __hadd2(a, b);
+  const __half2 A = __habs2(a), B = __habs2(b), S = __habs2(s);
+  const __half2 q = __hsub2_sat(B, A);    // [|b| > |a|]
+  const __half2 r1 = __hsub2_sat(B, S);   // [|b| > |s|]
+  const __half2 r2 = __hsub2_sat(S, A);   // [|s| > |a|]
+  const __half2 u1 = __hsub2(__float2half2_rn(1.f), q);
+  const __half2 itl = __hfma2(u1, __hneg2(r1), u1);   // (1 - q)(1 - r1)
+  const __half2 itr = __hmul2(q, r2);
+  return h22u(__hfma2(b, itr, __hfma2(a, itl, T)));
+}
+
+// Which predictor pairs run paeth_h2 (FMA pipes) instead of paeth_pred2 (ALU + IMAD), to balance the
+// two half-rate pipes: bit 2*parity + pair, parity 0 = the odd rows r of the two-row loop, 1 = r + 1;
+// pair 0 = columns j4, j4+1, pair 1 = j4+2, j4+3. Any non-zero mask keeps every sample as a biased half
+// (paeth_pred2 carries the bias through: its unused result bytes come from TR's high byte).
+#ifndef L3_H2_F32
+#define L3_H2_F32 0xF   // fp32 planar / crop paths
+#endif
+#ifndef L3_H2_U8
+#define L3_H2_U8 0xF    // u8 planar / crop paths (0: the byte-form paeth_pred4)
+#endif
+#ifndef L3_UNPACK_SHF
+#define L3_UNPACK_SHF 1   // fp32 delta unpack: 0 = left shifts as IMAD, 1 = as SHF (u8 paths keep IMAD)
+#endif
+#ifndef L3_H2_CVT
+#define L3_H2_CVT 0     // fp32 stores of biased halves: 1 = HADD2 + HADD2.F32 (FMA pipes), 0 = I2F.U8 (XU)
+#endif
+
 #ifndef L3_U8_V16
 #define L3_U8_V16 0   // A/B: u8 rows as 128-bit stores (4-lane shuffle gather) where aligned; measured slower
 #endif
 #ifndef L3_MIN_CTAS
 #define L3_MIN_CTAS 6   // __launch_bounds__ min CTAs per SM for the planar kernels: register cap 80, no spills
+#endif
+#ifndef L3_CROP_MIN_CTAS
+#define L3_CROP_MIN_CTAS 0   // crop (f3) kernels: no register cap (96 registers, 5 CTAs per SM)
 #endif
 #ifndef L3_SMEM_PREFIX
 #define L3_SMEM_PREFIX 1   // per-CTA shared-memory copy of the task prefix for the image lookup (n <= 256)
@@ -269,11 +313,23 @@ struct LaneRows {
 
 // FAST: aligned vector store. Otherwise scalar stores; RAGGED: the patch width is not a multiple of
 // 4, so the lane's trailing columns may lie outside it (else all 4 are stored unconditionally).
-template <bool F32, bool FAST, bool RAGGED = !FAST>
+// H2: biased-half pairs (0x6400 | c per half): c = (1024 + c) - 1024 by one HADD2 per pair, then the
+// fp16 -> fp32 conversion (HADD2.F32) and the normalise FFMA, all off the ALU pipe.
+template <bool F32, bool FAST, bool RAGGED = !FAST, bool H2 = false>
 __device__ __forceinline__ void store4(const LaneRows& s, uint32_t xA, uint32_t xB, float sc, float bi, bool pred) {
   if (F32) {
-    const float v0 = fmaf((float)(xA & 0xFFFFu), sc, bi), v1 = fmaf((float)(xA >> 16), sc, bi);
-    const float v2 = fmaf((float)(xB & 0xFFFFu), sc, bi), v3 = fmaf((float)(xB >> 16), sc, bi);
+    float c0, c1, c2, c3;
+    if (H2 && L3_H2_CVT) {
+      const float2 fa = __half22float2(__hsub2(u2h2(xA), __float2half2_rn(1024.f)));
+      const float2 fb = __half22float2(__hsub2(u2h2(xB), __float2half2_rn(1024.f)));
+      c0 = fa.x; c1 = fa.y; c2 = fb.x; c3 = fb.y;
+    } else if (H2) {
+      c0 = (float)(xA & 0xFFu); c1 = (float)((xA >> 16) & 0xFFu); c2 = (float)(xB & 0xFFu); c3 = (float)((xB >> 16) & 0xFFu);
+    } else {
+      c0 = (float)(xA & 0xFFFFu); c1 = (float)(xA >> 16); c2 = (float)(xB & 0xFFFFu); c3 = (float)(xB >> 16);
+    }
+    const float v0 = fmaf(c0, sc, bi), v1 = fmaf(c1, sc, bi);
+    const float v2 = fmaf(c2, sc, bi), v3 = fmaf(c3, sc, bi);
     if (FAST) {   // predicated STG.128, no branch
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
@@ -374,7 +430,7 @@ __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
 // STORE = false (HWC kernel): the row's pixels are left in s.A / s.B for an interleaving store.
 template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP, bool STORE = true, int SLOTS = kSlots,
-          bool HWC = false, bool RAGGED = !FAST>
+          bool HWC = false, bool RAGGED = !FAST, int PAR = 0>
 __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
   const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
@@ -388,15 +444,30 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   // a4: pixel-wise delta unpack (PAPER.md:152 step 2, :187): field = 4 k-bit deltas, MSB-first
   const uint32_t field = rbits<SLOTS>(ring, s.bp + 12u + s.j4 * k);
   const uint32_t sh = 32u - k;
-  const uint32_t pk = shl_c(1u, k);
   const uint32_t d0 = shr_c(field, sh);
-  const uint32_t d1 = shr_c(field * pk, sh);
-  const uint32_t d2 = shr_c(field * (pk * pk), sh);
-  const uint32_t d3 = shr_c(field * (pk * pk * pk), sh);
+  uint32_t d1, d2, d3;
+#if L3_UNPACK_SHF
+  if (F32) {   // the left shifts on the ALU pipe (balances the FMA-pipe-heavy fp32 predictor mix)
+  d1 = shr_c(shl_c(field, k), sh);
+  d2 = shr_c(shl_c(field, 2u * k), sh);
+  d3 = shr_c(shl_c(field, 3u * k), sh);
+  } else
+#endif
+  {             // the left shifts as multiplies (IMAD, FMA pipe)
+  const uint32_t pk = shl_c(1u, k);
+  d1 = shr_c(field * pk, sh);
+  d2 = shr_c(field * (pk * pk), sh);
+  d3 = shr_c(field * (pk * pk * pk), sh);
+  }
   const uint32_t dA = d1 * 0x10000u + d0 + base2;
   const uint32_t dB = d3 * 0x10000u + d2 + base2;
   // byte-form predictor: u8 planar / crop stores (measured: C2 -1.7 %, C3 u8 neutral, fp32 +5 %)
-  constexpr bool P4 = STORE && !F32 && (L3_PRED4 != 0);
+  constexpr bool P4 = STORE && !F32 && (L3_PRED4 != 0) && (L3_H2_U8 == 0);
+  // biased-half pair form (paeth_h2): halves hold 0x6400 | c instead of c
+  constexpr int kH2Mask = STORE ? (F32 ? L3_H2_F32 : L3_H2_U8) : 0;
+  constexpr bool H2 = kH2Mask != 0;
+  constexpr int HM = (kH2Mask >> (2 * PAR)) & 3;
+  constexpr uint32_t kBias = H2 ? 0x64006400u : 0u;
   uint32_t xA, xB;
   if (P4) {
     if (FIRST) {
@@ -419,8 +490,8 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     s.Q = q;
   } else {
   if (FIRST) {
-    xA = dA & 0x00FF00FFu;
-    xB = dB & 0x00FF00FFu;
+    xA = (dA & 0x00FF00FFu) | kBias;
+    xB = (dB & 0x00FF00FFu) | kBias;
   } else {
     // a5: row-wise parallel custom Paeth
     const uint32_t Bl = __shfl_up_sync(0xffffffffu, s.B, 1, Lw);     // left lane's (c2, c3)
@@ -437,20 +508,27 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     const uint32_t TRA = prmt(s.A, s.B, 0x5412);      // (c1, c2) = TL of pair B
     const uint32_t TRB = prmt(s.B, RT, 0x5412);       // (c3, c+4)
 #endif
-    xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
-    xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
+    if (H2) {   // (0x6400 | pred) + residual + (k:4 | base:8): keep the low byte, restore the bias
+      const uint32_t pA = (HM & 1) ? paeth_h2(TLA, s.A, TRA) : paeth_pred2(TLA, s.A, TRA, K);
+      const uint32_t pB = (HM & 2) ? paeth_h2(TRA, s.B, TRB) : paeth_pred2(TRA, s.B, TRB, K);
+      xA = ((pA + dA) & 0x00FF00FFu) | kBias;
+      xB = ((pB + dB) & 0x00FF00FFu) | kBias;
+    } else {
+      xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
+      xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
+    }
   }
   if (RAGGED) {   // ragged patch: columns >= w are ghosts of column w-1
-    if (s.j4 + 1 >= s.w) xA = (xA & 0xFFu) * 0x00010001u;
+    if (s.j4 + 1 >= s.w) xA = (xA & 0xFFFFu) * 0x00010001u;
     if (s.j4 + 2 >= s.w) xB = (xA >> 16) * 0x00010001u;
-    if (s.j4 + 3 >= s.w) xB = (xB & 0xFFu) * 0x00010001u;
+    if (s.j4 + 3 >= s.w) xB = (xB & 0xFFFFu) * 0x00010001u;
   }
   // a6: store (u8 planar, or fused cast + normalise)
   if (!STORE) {
   } else if (CROP) {
     store4_crop<F32, HWC>(s, xA, xB, sc, bi, live);
   } else {
-    store4<F32, FAST, RAGGED>(s, xA, xB, sc, bi, live && s.valid);
+    store4<F32, FAST, RAGGED, H2>(s, xA, xB, sc, bi, live && s.valid);
   }
   s.A = xA;
   s.B = xB;
@@ -483,8 +561,8 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r, Lw, sc, bi, K);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r + 1, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
@@ -524,7 +602,7 @@ namespace l3 {
 // for 33 <= N <= 128 and runs at 4 CTAs per SM.
 // HWC (with CROP only): the augment variant writes the window interleaved [h, w, 3].
 template <bool F32, bool WIDE, bool CROP, bool HWC = false>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? 0 : L3_MIN_CTAS))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_MIN_CTAS : L3_MIN_CTAS))
     l3_decode_kernel(DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned int ticket;

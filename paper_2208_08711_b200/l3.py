@@ -105,6 +105,8 @@ def lib() -> ctypes.CDLL:
             L.l3_selftest_paeth.restype = ctypes.c_int
             L.l3_selftest_paeth4.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
             L.l3_selftest_paeth4.restype = ctypes.c_int
+            L.l3_selftest_paeth_h2.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+            L.l3_selftest_paeth_h2.restype = ctypes.c_int
             L.l3_status_string.argtypes = [ctypes.c_int32]
             L.l3_status_string.restype = ctypes.c_char_p
             L.l3_choose_patch_size.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
@@ -122,7 +124,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("l3_decode_workspace_size", "l3_decode_batch", "l3_parse_batch",
             "l3_load_decode_batch", "l3_decode_kernels_per_call", "l3_status_string", "l3_choose_patch_size",
             "l3_encode_max_bytes", "l3_encode_workspace_size", "l3_encode_batch", "l3_selftest_paeth",
-            "l3_selftest_paeth4", "l3_decode_batch_ablation")
+            "l3_selftest_paeth4", "l3_selftest_paeth_h2", "l3_decode_batch_ablation")
 
 
 def _dev_ptr(t: torch.Tensor | None, name: str, dtype=None) -> int:
@@ -215,6 +217,12 @@ def l3_selftest_paeth4(out: torch.Tensor, stream=None) -> None:
     if out.numel() < (4 << 24):
         raise ValueError("out needs 4 * 2^24 bytes")
     _check("l3_selftest_paeth4", lib().l3_selftest_paeth4(_dev_ptr(out, "out", torch.uint8), _stream(stream)))
+
+
+def l3_selftest_paeth_h2(out: torch.Tensor, stream=None) -> None:
+    if out.numel() < (1 << 24):
+        raise ValueError("out needs 2^24 bytes")
+    _check("l3_selftest_paeth_h2", lib().l3_selftest_paeth_h2(_dev_ptr(out, "out", torch.uint8), _stream(stream)))
 
 
 def l3_status_string(status: int) -> str:

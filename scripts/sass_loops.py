@@ -43,7 +43,7 @@ def row_loops(ins: list[tuple[int, str]]):
         tgt = int(m.group(1), 16)
         if tgt < a and tgt in addr:
             body = ins[addr[tgt]:i + 1]
-            if any("VIMNMX3" in x for _, x in body) and len(body) < 800:
+            if any(("VIMNMX3" in x or "HMUL2" in x) for _, x in body) and len(body) < 800:
                 yield tgt, a, body
 
 
@@ -57,7 +57,7 @@ def main() -> None:
         for tgt, a, body in row_loops(ins):
             ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", x).split()[0] for _, x in body)
             print(f"  loop {tgt:#x}-{a:#x}: {len(body)} instr, VIMNMX3 x{ops['VIMNMX3.U16x2']}, "
-                  f"LDL/STL {ops['LDL'] + ops['STL']}")
+                  f"HMUL2 x{ops['HMUL2']}, LDL/STL {ops['LDL'] + ops['STL']}")
             print("    " + ", ".join(f"{k} {v}" for k, v in ops.most_common(14)))
 
 
@@ -87,3 +87,25 @@ def pipe_mix(body) -> dict[str, int]:
         else:
             mix["other"] += 1
     return dict(mix)
+
+
+def mix_report(lib: str, pat: str) -> None:
+    """ALU / FMA-class / other op counts of each row loop (python -c 'import scripts.sass_loops as s; ...')."""
+    half = ("HADD2", "HFMA2", "HMUL2")
+    for name, ins in functions(lib).items():
+        if pat not in name:
+            continue
+        for tgt, a, body in row_loops(ins):
+            c = collections.Counter()
+            for _, x in body:
+                op = re.sub(r"^@!?U?P\w+\s+", "", x).split()[0]
+                b = op.split(".")[0]
+                if b in ALU or op.startswith("VIMNMX") or op.startswith("VIADD"):
+                    c["alu"] += 1
+                elif b in FMA:
+                    c["fma"] += 1
+                elif b in half:
+                    c["half"] += 1
+                else:
+                    c["other"] += 1
+            print(f"{name[:60]} {tgt:#x}: {len(body)} instr {dict(c)}")

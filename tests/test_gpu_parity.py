@@ -268,6 +268,20 @@ def test_device_predictor_exhaustive_2_24():
     assert bad.size == 0, [(int(i) >> 16, (int(i) >> 8) & 255, int(i) & 255, int(got[i]), int(ref[i])) for i in bad[:8]]
 
 
+def test_device_predictor_h2_exhaustive_2_24():
+    """The kernel's biased-half (fp16x2) predictor equals the oracle on all 2^24 triples."""
+    from paper_2208_08711_b200 import l3
+    out = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+    l3.l3_selftest_paeth_h2(out)
+    torch.cuda.synchronize()
+    idx = np.arange(1 << 24, dtype=np.uint32)
+    ref = l3ref.predict_many((idx >> 16).astype(np.uint8), ((idx >> 8) & 255).astype(np.uint8),
+                             (idx & 255).astype(np.uint8))
+    got = out.cpu().numpy()
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, [(int(i) >> 16, (int(i) >> 8) & 255, int(i) & 255, int(got[i]), int(ref[i])) for i in bad[:8]]
+
+
 def test_device_predictor4_exhaustive_2_24():
     """The kernel's byte-form 4-sample predictor equals the oracle on all 2^24 triples,
     at each of the 4 sample positions of a lane (neighbouring columns hashed)."""
