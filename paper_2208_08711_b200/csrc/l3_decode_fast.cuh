@@ -227,6 +227,22 @@ __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t t
 #ifndef L3_H2_U8
 #define L3_H2_U8 0xF    // u8 planar / crop paths (0: the byte-form paeth_pred4)
 #endif
+#ifndef L3_H2_WIDE
+#define L3_H2_WIDE 5    // u8 wide 8-column path: bit i = pair i of the lane's 4 pairs runs paeth_h2 (C4 -1.1 %)
+#endif
+#ifndef L3_UNPACK_TAB
+#define L3_UNPACK_TAB 0   // delta unpack by shift amounts / mask from a per-k shared table (A/B option)
+#endif
+// Per-k unpack table (L3_UNPACK_TAB): {32 - k, 16 - 2k, 2k, ((1 << k) - 1) << 16} for k = 1..8, zeros for the
+// invalid k (their rows are flagged by the validity accumulator). Every kernel that runs decode_row fills it.
+__shared__ uint4 l3_ktab[16];
+__device__ __forceinline__ void init_ktab() {
+  if (threadIdx.x < 16) {
+    const uint32_t k = threadIdx.x;
+    l3_ktab[k] = (k >= 1 && k <= 8) ? make_uint4(32u - k, 16u - 2u * k, 2u * k, ((1u << k) - 1u) << 16)
+                                    : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
 #ifndef L3_UNPACK_SHF
 #define L3_UNPACK_SHF 1   // fp32 delta unpack: 0 = left shifts as IMAD, 1 = as SHF (u8 paths keep IMAD)
 #endif
@@ -443,6 +459,15 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   const uint32_t raw_next = rbits<SLOTS>(ring, nbp);    // next row's header, fetched early
   // a4: pixel-wise delta unpack (PAPER.md:152 step 2, :187): field = 4 k-bit deltas, MSB-first
   const uint32_t field = rbits<SLOTS>(ring, s.bp + 12u + s.j4 * k);
+#if L3_UNPACK_TAB
+  // the row's shift amounts and mask from the per-k table (one broadcast LDS.128, issued beside the
+  // field's loads): dA = (d1 << 16) | d0 from field >> (16 - 2k) (d1 lands at bit 16) and
+  // field >> (32 - k); dB the same from field << 2k
+  const uint4 T = l3_ktab[k];
+  const uint32_t g = shl_c(field, T.z);
+  const uint32_t dA = ((shr_c(field, T.y) & T.w) | shr_c(field, T.x)) + base2;
+  const uint32_t dB = ((shr_c(g, T.y) & T.w) | shr_c(g, T.x)) + base2;
+#else
   const uint32_t sh = 32u - k;
   const uint32_t d0 = shr_c(field, sh);
   uint32_t d1, d2, d3;
@@ -461,6 +486,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   }
   const uint32_t dA = d1 * 0x10000u + d0 + base2;
   const uint32_t dB = d3 * 0x10000u + d2 + base2;
+#endif
   // byte-form predictor: u8 planar / crop stores (measured: C2 -1.7 %, C3 u8 neutral, fp32 +5 %)
   constexpr bool P4 = STORE && !F32 && (L3_PRED4 != 0) && (L3_H2_U8 == 0);
   // biased-half pair form (paeth_h2): halves hold 0x6400 | c instead of c
@@ -612,6 +638,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   if (lane == 0) {
     for (int s = 0; s < kSlots; s++) mbar_init(&bars[s], 1);
     fence_mbar_init();
+  }
+  if (L3_UNPACK_TAB) {
+    init_ktab();
+    __syncthreads();
   }
   __syncwarp();
   uint32_t phase_bits = 0;

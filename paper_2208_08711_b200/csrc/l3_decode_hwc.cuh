@@ -427,6 +427,10 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     for (int s = 0; s < 3 * kHwcSlots; s++) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
+  if (L3_UNPACK_TAB) {
+    init_ktab();
+    __syncthreads();
+  }
   __syncwarp();
   uint32_t ph[3] = {0u, 0u, 0u};
   WsHead* head = p.pp.ws.head;

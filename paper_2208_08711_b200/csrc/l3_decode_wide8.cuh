@@ -237,11 +237,15 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
     s.optr += s.pitch;
     return;
   }
+  // which of the 4 pairs run the biased-half predictor (paeth_h2, FMA pipes; bit i = pair i); any
+  // non-zero mask keeps every sample as a biased half 0x6400 | c (l3_decode_fast.cuh)
+  constexpr int kH2 = F32 ? 0 : L3_H2_WIDE;
+  constexpr uint32_t kBias = kH2 ? 0x64006400u : 0u;
   if (FIRST) {
-    xA = dA & 0x00FF00FFu;
-    xB = dB & 0x00FF00FFu;
-    xC = dC & 0x00FF00FFu;
-    xD = dD & 0x00FF00FFu;
+    xA = (dA & 0x00FF00FFu) | kBias;
+    xB = (dB & 0x00FF00FFu) | kBias;
+    xC = (dC & 0x00FF00FFu) | kBias;
+    xD = (dD & 0x00FF00FFu) | kBias;
   } else {
     // a5: row-wise parallel custom Paeth, 4 pairs
     const uint32_t Dl = __shfl_up_sync(0xffffffffu, s.D, 1, L);     // left lane's (c6, c7)
@@ -253,20 +257,25 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
     const uint32_t TRB = prmt(s.B, s.C, 0x5412);
     const uint32_t TRC = prmt(s.C, s.D, 0x5412);
     const uint32_t TRD = prmt(s.D, RT, 0x5412);
-    xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
-    xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
-    xC = (paeth_pred2(TRB, s.C, TRC, K) + dC) & 0x00FF00FFu;
-    xD = (paeth_pred2(TRC, s.D, TRD, K) + dD) & 0x00FF00FFu;
+    const uint32_t pA = (kH2 & 1) ? paeth_h2(TLA, s.A, TRA) : paeth_pred2(TLA, s.A, TRA, K);
+    const uint32_t pB = (kH2 & 2) ? paeth_h2(TRA, s.B, TRB) : paeth_pred2(TRA, s.B, TRB, K);
+    const uint32_t pC = (kH2 & 4) ? paeth_h2(TRB, s.C, TRC) : paeth_pred2(TRB, s.C, TRC, K);
+    const uint32_t pD = (kH2 & 8) ? paeth_h2(TRC, s.D, TRD) : paeth_pred2(TRC, s.D, TRD, K);
+    xA = ((pA + dA) & 0x00FF00FFu) | kBias;
+    xB = ((pB + dB) & 0x00FF00FFu) | kBias;
+    xC = ((pC + dC) & 0x00FF00FFu) | kBias;
+    xD = ((pD + dD) & 0x00FF00FFu) | kBias;
   }
   if (!FAST) {   // ragged patch: columns >= w are ghosts of column w-1
-    uint32_t x[8] = {xA & 0xFFu, xA >> 16, xB & 0xFFu, xB >> 16, xC & 0xFFu, xC >> 16, xD & 0xFFu, xD >> 16};
+    uint32_t x[8] = {xA & 0xFFu, (xA >> 16) & 0xFFu, xB & 0xFFu, (xB >> 16) & 0xFFu,
+                     xC & 0xFFu, (xC >> 16) & 0xFFu, xD & 0xFFu, (xD >> 16) & 0xFFu};
 #pragma unroll
     for (int c = 1; c < 8; c++)
       if (s.j8 + c >= s.w) x[c] = x[c - 1];
-    xA = x[0] | (x[1] << 16);
-    xB = x[2] | (x[3] << 16);
-    xC = x[4] | (x[5] << 16);
-    xD = x[6] | (x[7] << 16);
+    xA = x[0] | (x[1] << 16) | kBias;
+    xB = x[2] | (x[3] << 16) | kBias;
+    xC = x[4] | (x[5] << 16) | kBias;
+    xD = x[6] | (x[7] << 16) | kBias;
   }
   store8<F32, FAST>(s, xA, xB, xC, xD, sc, bi, live && s.valid, L);
   s.A = xA;
