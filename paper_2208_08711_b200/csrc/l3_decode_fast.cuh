@@ -231,7 +231,7 @@ __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t t
 #define L3_H2_WIDE 5    // u8 wide 8-column path: bit i = pair i of the lane's 4 pairs runs paeth_h2 (C4 -1.1 %)
 #endif
 #ifndef L3_UNPACK_TAB
-#define L3_UNPACK_TAB 0   // delta unpack by shift amounts / mask from a per-k shared table (A/B option)
+#define L3_UNPACK_TAB 1   // delta unpack by shift amounts / mask from a per-k shared table (C3 u8 -2.5 %, fp32 -1.2 %)
 #endif
 // Per-k unpack table (L3_UNPACK_TAB): {32 - k, 16 - 2k, 2k, ((1 << k) - 1) << 16} for k = 1..8, zeros for the
 // invalid k (their rows are flagged by the validity accumulator). Every kernel that runs decode_row fills it.
