@@ -221,6 +221,22 @@ __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t t
 // two half-rate pipes: bit 2*parity + pair, parity 0 = the odd rows r of the two-row loop, 1 = r + 1;
 // pair 0 = columns j4, j4+1, pair 1 = j4+2, j4+3. Any non-zero mask keeps every sample as a biased half
 // (paeth_pred2 carries the bias through: its unused result bytes come from TR's high byte).
+// (x & 0x00FF00FF) | bias as ONE LOP3: the bias arrives in a register (bias_reg) so ptxas cannot split
+// the two constants into two LOP3s. bias_reg(K) = K * 0xC800C8 = 0x64006400 for the run-time K = 128.
+#ifndef L3_BIAS_LOP3
+#define L3_BIAS_LOP3 1
+#endif
+__device__ __forceinline__ uint32_t bias_reg(uint32_t K) { return K * 0x00C800C8u; }
+__device__ __forceinline__ uint32_t lo_bytes_biased(uint32_t x, uint32_t bias) {
+#if L3_BIAS_LOP3
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x00FF00FF, %2, 0xEA;" : "=r"(d) : "r"(x), "r"(bias));   // (a & b) | c
+  return d;
+#else
+  return (x & 0x00FF00FFu) | 0x64006400u;
+#endif
+}
+
 #ifndef L3_H2_F32
 #define L3_H2_F32 0xF   // fp32 planar / crop paths
 #endif
@@ -230,12 +246,24 @@ __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t t
 #ifndef L3_H2_WIDE
 #define L3_H2_WIDE 5    // u8 wide 8-column path: bit i = pair i of the lane's 4 pairs runs paeth_h2 (C4 -1.1 %)
 #endif
+#ifndef L3_REFILL_AHEAD
+#define L3_REFILL_AHEAD 2048   // streamed ring: land 2 KB beyond the next two rows per refill call (fewer calls)
+#endif
 #ifndef L3_UNPACK_TAB
 #define L3_UNPACK_TAB 1   // delta unpack by shift amounts / mask from a per-k shared table (C3 u8 -2.5 %, fp32 -1.2 %)
 #endif
 // Per-k unpack table (L3_UNPACK_TAB): {32 - k, 16 - 2k, 2k, ((1 << k) - 1) << 16} for k = 1..8, zeros for the
 // invalid k (their rows are flagged by the validity accumulator). Every kernel that runs decode_row fills it.
 __shared__ uint4 l3_ktab[16];
+// Table entry k by a 32-bit shared-window address (ld.shared): the generic-pointer form made ptxas
+// rebuild the entry's cluster-window address (S2R SR_CgaCtaId + 3 ops) in every row.
+__device__ __forceinline__ uint4 ktab_entry(uint32_t k) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"((uint32_t)__cvta_generic_to_shared(l3_ktab) + 16u * k));
+  return v;
+}
 __device__ __forceinline__ void init_ktab() {
   if (threadIdx.x < 16) {
     const uint32_t k = threadIdx.x;
@@ -463,7 +491,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   // the row's shift amounts and mask from the per-k table (one broadcast LDS.128, issued beside the
   // field's loads): dA = (d1 << 16) | d0 from field >> (16 - 2k) (d1 lands at bit 16) and
   // field >> (32 - k); dB the same from field << 2k
-  const uint4 T = l3_ktab[k];
+  const uint4 T = ktab_entry(k);
   const uint32_t g = shl_c(field, T.z);
   const uint32_t dA = ((shr_c(field, T.y) & T.w) | shr_c(field, T.x)) + base2;
   const uint32_t dB = ((shr_c(g, T.y) & T.w) | shr_c(g, T.x)) + base2;
@@ -493,7 +521,6 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   constexpr int kH2Mask = STORE ? (F32 ? L3_H2_F32 : L3_H2_U8) : 0;
   constexpr bool H2 = kH2Mask != 0;
   constexpr int HM = (kH2Mask >> (2 * PAR)) & 3;
-  constexpr uint32_t kBias = H2 ? 0x64006400u : 0u;
   uint32_t xA, xB;
   if (P4) {
     if (FIRST) {
@@ -516,8 +543,8 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     s.Q = q;
   } else {
   if (FIRST) {
-    xA = (dA & 0x00FF00FFu) | kBias;
-    xB = (dB & 0x00FF00FFu) | kBias;
+    xA = H2 ? lo_bytes_biased(dA, bias_reg(K)) : (dA & 0x00FF00FFu);
+    xB = H2 ? lo_bytes_biased(dB, bias_reg(K)) : (dB & 0x00FF00FFu);
   } else {
     // a5: row-wise parallel custom Paeth
     const uint32_t Bl = __shfl_up_sync(0xffffffffu, s.B, 1, Lw);     // left lane's (c2, c3)
@@ -537,8 +564,8 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
     if (H2) {   // (0x6400 | pred) + residual + (k:4 | base:8): keep the low byte, restore the bias
       const uint32_t pA = (HM & 1) ? paeth_h2(TLA, s.A, TRA) : paeth_pred2(TLA, s.A, TRA, K);
       const uint32_t pB = (HM & 2) ? paeth_h2(TRA, s.B, TRB) : paeth_pred2(TRA, s.B, TRB, K);
-      xA = ((pA + dA) & 0x00FF00FFu) | kBias;
-      xB = ((pB + dB) & 0x00FF00FFu) | kBias;
+      xA = lo_bytes_biased(pA + dA, bias_reg(K));
+      xB = lo_bytes_biased(pB + dB, bias_reg(K));
     } else {
       xA = (paeth_pred2(TLA, s.A, TRA, K) + dA) & 0x00FF00FFu;
       xB = (paeth_pred2(TRA, s.B, TRB, K) + dB) & 0x00FF00FFu;
@@ -580,13 +607,15 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
                                                  uint32_t rowmax, int lane) {
   constexpr bool GUARD = !STREAM;   // G == 1: every lane runs exactly the unit's h rows
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-    stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
+    stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
+                   lane);
   s.raw = rbits(ring, s.bp);
   decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax, lane);
+      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
+                     lane);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0>(s, ring, r, Lw, sc, bi, K);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1>(s, ring, r + 1, Lw, sc, bi, K);
   }

@@ -242,10 +242,10 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
   constexpr int kH2 = F32 ? 0 : L3_H2_WIDE;
   constexpr uint32_t kBias = kH2 ? 0x64006400u : 0u;
   if (FIRST) {
-    xA = (dA & 0x00FF00FFu) | kBias;
-    xB = (dB & 0x00FF00FFu) | kBias;
-    xC = (dC & 0x00FF00FFu) | kBias;
-    xD = (dD & 0x00FF00FFu) | kBias;
+    xA = kH2 ? lo_bytes_biased(dA, bias_reg(K)) : (dA & 0x00FF00FFu);
+    xB = kH2 ? lo_bytes_biased(dB, bias_reg(K)) : (dB & 0x00FF00FFu);
+    xC = kH2 ? lo_bytes_biased(dC, bias_reg(K)) : (dC & 0x00FF00FFu);
+    xD = kH2 ? lo_bytes_biased(dD, bias_reg(K)) : (dD & 0x00FF00FFu);
   } else {
     // a5: row-wise parallel custom Paeth, 4 pairs
     const uint32_t Dl = __shfl_up_sync(0xffffffffu, s.D, 1, L);     // left lane's (c6, c7)
@@ -261,10 +261,10 @@ __device__ __forceinline__ void decode_row8(Lane8& s, const uint8_t* ring, uint3
     const uint32_t pB = (kH2 & 2) ? paeth_h2(TRA, s.B, TRB) : paeth_pred2(TRA, s.B, TRB, K);
     const uint32_t pC = (kH2 & 4) ? paeth_h2(TRB, s.C, TRC) : paeth_pred2(TRB, s.C, TRC, K);
     const uint32_t pD = (kH2 & 8) ? paeth_h2(TRC, s.D, TRD) : paeth_pred2(TRC, s.D, TRD, K);
-    xA = ((pA + dA) & 0x00FF00FFu) | kBias;
-    xB = ((pB + dB) & 0x00FF00FFu) | kBias;
-    xC = ((pC + dC) & 0x00FF00FFu) | kBias;
-    xD = ((pD + dD) & 0x00FF00FFu) | kBias;
+    xA = kH2 ? lo_bytes_biased(pA + dA, bias_reg(K)) : ((pA + dA) & 0x00FF00FFu);
+    xB = kH2 ? lo_bytes_biased(pB + dB, bias_reg(K)) : ((pB + dB) & 0x00FF00FFu);
+    xC = kH2 ? lo_bytes_biased(pC + dC, bias_reg(K)) : ((pC + dC) & 0x00FF00FFu);
+    xD = kH2 ? lo_bytes_biased(pD + dD, bias_reg(K)) : ((pD + dD) & 0x00FF00FFu);
   }
   if (!FAST) {   // ragged patch: columns >= w are ghosts of column w-1
     uint32_t x[8] = {xA & 0xFFu, (xA >> 16) & 0xFFu, xB & 0xFFu, (xB >> 16) & 0xFFu,
