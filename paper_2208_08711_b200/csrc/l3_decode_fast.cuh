@@ -274,6 +274,9 @@ __device__ __forceinline__ void init_ktab() {
 #ifndef L3_UNPACK_SHF
 #define L3_UNPACK_SHF 1   // fp32 delta unpack: 0 = left shifts as IMAD, 1 = as SHF (u8 paths keep IMAD)
 #endif
+#ifndef L3_H2_HWC
+#define L3_H2_HWC 0xF   // HWC tile kernel (rows left in s.A / s.B for the interleaving store): C3 HWC -7 %
+#endif
 #ifndef L3_H2_CVT
 #define L3_H2_CVT 0     // fp32 stores of biased halves: 1 = HADD2 + HADD2.F32 (FMA pipes), 0 = I2F.U8 (XU)
 #endif
@@ -518,7 +521,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   // byte-form predictor: u8 planar / crop stores (measured: C2 -1.7 %, C3 u8 neutral, fp32 +5 %)
   constexpr bool P4 = STORE && !F32 && (L3_PRED4 != 0) && (L3_H2_U8 == 0);
   // biased-half pair form (paeth_h2): halves hold 0x6400 | c instead of c
-  constexpr int kH2Mask = STORE ? (F32 ? L3_H2_F32 : L3_H2_U8) : 0;
+  constexpr int kH2Mask = STORE ? (F32 ? L3_H2_F32 : L3_H2_U8) : L3_H2_HWC;
   constexpr bool H2 = kH2Mask != 0;
   constexpr int HM = (kH2Mask >> (2 * PAR)) & 3;
   uint32_t xA, xB;

@@ -123,7 +123,8 @@ __device__ __forceinline__ void store12(uint8_t* optr, const LaneRows& r, const 
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         const uint32_t pr = x[c][t >> 1];
-        v[3 * t + c] = fmaf((float)((t & 1) ? (pr >> 16) : (pr & 0xFFFFu)), sc[c], bi[c]);
+        // the low byte of each half (the pair may hold biased halves 0x6400 | c, L3_H2_HWC)
+        v[3 * t + c] = fmaf((float)((t & 1) ? ((pr >> 16) & 0xFFu) : (pr & 0xFFu)), sc[c], bi[c]);
       }
     if (MODE == kStAligned) {
 #pragma unroll
