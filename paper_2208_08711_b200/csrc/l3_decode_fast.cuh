@@ -197,17 +197,26 @@ __device__ __forceinline__ uint32_t paeth_pred2(uint32_t tl, uint32_t t, uint32_
 // BIASED HALVES: each 16-bit half is the fp16 value 1024 + c (bits 0x6400 | c), so differences are exact
 // small integers and the bits stay an integer pair for the mod-256 residual add. With a = TL - T,
 // b = TR - T, s = a + b the distances are d(TL) = |b|, d(T) = |s|, d(TR) = |a|, and for
-// integers sat(x - y) = [x > y]. TL wins iff |b| <= |a| and |b| <= |s|; TR iff |a| < |b| and |a| < |s|;
-// else T. So pred = T + a·[TL wins] + b·[TR wins] = 11 HADD2 / HFMA2 / HMUL2 (|x| and .SAT are operand
-// and result modifiers): the predictor runs on the FMA / FP16 pipes instead of the half-rate ALU pipe.
+// integers sat(x - y) = [x > y]. TL wins iff |b| <= min(|a|, |s|), i.e. x1 = sat(|b| - min(|a|, |s|)) = 0;
+// TR wins iff |a| < min(|b|, |s|), i.e. r = sat(min(|b|, |s|) - |a|) = 1; else T. So
+// pred = (TL - a·x1) + b·r: x1 = 0 gives TL, x1 = 1 gives T, plus b when TR wins (then x1 = 1). That is
+// 7 HADD2 / HFMA2 on the FMA pipes and 2 HMNMX2 on the ALU (|x| and .SAT fold into the instructions).
 // Every intermediate is an integer of magnitude <= 1534 (exact in fp16). DESIGN.md §5;
 // exhaustively checked by l3_selftest_paeth_h2.
 __device__ __forceinline__ __half2 u2h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 __device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+#ifndef L3_H2_MIN
+#define L3_H2_MIN 1   // 1: the 9-op form with two HMNMX2; 0: the 11-op all-FMA-pipe form
+#endif
 __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t tr) {
   const __half2 TL = u2h2(tl), T = u2h2(t), TR = u2h2(tr);
   const __half2 a = __hsub2(TL, T), b = __hsub2(TR, T), s = __hadd2(a, b);
   const __half2 A = __habs2(a), B = __habs2(b), S = __habs2(s);
+#if L3_H2_MIN
+  const __half2 x1 = __hsub2_sat(B, __hmin2(A, S));   // [TL does not win]
+  const __half2 r = __hsub2_sat(__hmin2(B, S), A);    // [TR wins]
+  return h22u(__hfma2(b, r, __hfma2(a, __hneg2(x1), TL)));
+#else
   const __half2 q = __hsub2_sat(B, A);    // [|b| > |a|]
   const __half2 r1 = __hsub2_sat(B, S);   // [|b| > |s|]
   const __half2 r2 = __hsub2_sat(S, A);   // [|s| > |a|]
@@ -215,14 +224,9 @@ __device__ __forceinline__ uint32_t paeth_h2(uint32_t tl, uint32_t t, uint32_t t
   const __half2 itl = __hfma2(u1, __hneg2(r1), u1);   // (1 - q)(1 - r1)
   const __half2 itr = __hmul2(q, r2);
   return h22u(__hfma2(b, itr, __hfma2(a, itl, T)));
+#endif
 }
 
-// Which predictor pairs run paeth_h2 (FMA pipes) instead of paeth_pred2 (ALU + IMAD), to balance the
-// two half-rate pipes: bit 2*parity + pair, parity 0 = the odd rows r of the two-row loop, 1 = r + 1;
-// pair 0 = columns j4, j4+1, pair 1 = j4+2, j4+3. Any non-zero mask keeps every sample as a biased half
-// (paeth_pred2 carries the bias through: its unused result bytes come from TR's high byte).
-// (x & 0x00FF00FF) | bias as ONE LOP3: the bias arrives in a register (bias_reg) so ptxas cannot split
-// the two constants into two LOP3s. bias_reg(K) = K * 0xC800C8 = 0x64006400 for the run-time K = 128.
 #ifndef L3_BIAS_LOP3
 #define L3_BIAS_LOP3 1
 #endif

@@ -43,7 +43,7 @@ def row_loops(ins: list[tuple[int, str]]):
         tgt = int(m.group(1), 16)
         if tgt < a and tgt in addr:
             body = ins[addr[tgt]:i + 1]
-            if any(("VIMNMX3" in x or "HMUL2" in x) for _, x in body) and len(body) < 800:
+            if any(("VIMNMX3" in x or "HMUL2" in x or "HMNMX2" in x) for _, x in body) and len(body) < 800:
                 yield tgt, a, body
 
 
@@ -91,7 +91,7 @@ def pipe_mix(body) -> dict[str, int]:
 
 def mix_report(lib: str, pat: str) -> None:
     """ALU / FMA-class / other op counts of each row loop (python -c 'import scripts.sass_loops as s; ...')."""
-    half = ("HADD2", "HFMA2", "HMUL2")
+    half = ("HADD2", "HFMA2", "HMUL2", "HMNMX2")
     for name, ins in functions(lib).items():
         if pat not in name:
             continue
