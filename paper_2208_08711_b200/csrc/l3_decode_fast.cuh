@@ -248,7 +248,7 @@ __device__ __forceinline__ uint32_t lo_bytes_biased(uint32_t x, uint32_t bias) {
 #define L3_H2_U8 0xF    // u8 planar / crop paths (0: the byte-form paeth_pred4)
 #endif
 #ifndef L3_H2_WIDE
-#define L3_H2_WIDE 5    // u8 wide 8-column path: bit i = pair i of the lane's 4 pairs runs paeth_h2 (C4 -1.1 %)
+#define L3_H2_WIDE 0xF  // u8 wide 8-column path: bit i = pair i of the lane's 4 pairs runs paeth_h2 (C4 -1.6 % vs 0x5)
 #endif
 #ifndef L3_REFILL_AHEAD
 #define L3_REFILL_AHEAD 2048   // streamed ring: land 2 KB beyond the next two rows per refill call (fewer calls)
