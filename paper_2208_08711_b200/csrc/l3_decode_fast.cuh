@@ -20,7 +20,14 @@
 
 namespace l3 {
 
-constexpr int kRingPitch = kRingBytes + 64;   // per-warp ring region (+ wrap mirrors)
+#ifndef L3_BULK_FIRST
+#define L3_BULK_FIRST 0   // planar streamed tasks: the first 8 KB of a unit as one bulk copy (measured slower)
+#endif
+#ifndef L3_KTAB_RING
+#define L3_KTAB_RING 1   // planar kernel: each warp's copy of the per-k unpack table sits after its ring
+#endif
+constexpr int kKtabOff = kRingBytes + 64;      // the table's offset in the warp's ring region
+constexpr int kRingPitch = kRingBytes + 64 + (L3_KTAB_RING ? 256 : 0);   // ring (+ wrap mirrors) + table
 
 __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -101,7 +108,21 @@ struct StreamState {
   uint64_t stage_end;   // absolute end of the bytes that matter
   uint32_t nchunks, issued, landed;
   uint32_t landed_end;  // A-relative bytes known to be resident (0xFFFFFFFF = all)
+  uint32_t group = 0;   // chunks [0, group) were issued as ONE bulk copy on bars[0] (L3_BULK_FIRST)
 };
+
+// Wait for chunk s.landed (the first chunk of the initial group waits for the whole group).
+template <int SLOTS = kSlots>
+__device__ __forceinline__ void stream_land(StreamState& s, uint64_t* bars, uint32_t& phase_bits) {
+  const uint32_t sl = s.landed % SLOTS;
+  if (s.landed >= s.group) {
+    mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
+    phase_bits ^= 1u << sl;
+  } else if (s.landed == 0) {
+    mbar_wait(&bars[0], phase_bits & 1u);
+    phase_bits ^= 1u;
+  }
+}
 
 template <int SLOTS = kSlots>
 __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
@@ -129,8 +150,7 @@ __device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim,
   }
   while (s.landed < s.issued && (uint64_t)s.landed * kSlotBytes < need) {
     const uint32_t sl = s.landed % SLOTS;
-    mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
-    phase_bits ^= 1u << sl;
+    stream_land<SLOTS>(s, bars, phase_bits);
     __syncwarp();
     swap_words(ring, sl * kSlotBytes, (sl + 1) * kSlotBytes, lane, 32);
     __syncwarp();
@@ -480,8 +500,10 @@ __device__ __forceinline__ void store4_crop(const LaneRows& s, uint32_t xA, uint
 // exact first error is re-derived after the patch (unit_first_error).
 // GUARD: rows may run past this lane's h (G > 1 segments of unequal height).
 // STORE = false (HWC kernel): the row's pixels are left in s.A / s.B for an interleaving store.
+// KT: 0 = the per-k table in the static shared array; else its byte offset from `ring` (the planar
+// kernel's per-warp copy, addressed from the ring's base register: no per-row address rebuild).
 template <bool FIRST, bool F32, bool FAST, bool GUARD, bool CROP, bool STORE = true, int SLOTS = kSlots,
-          bool HWC = false, bool RAGGED = !FAST, int PAR = 0>
+          bool HWC = false, bool RAGGED = !FAST, int PAR = 0, int KT = 0>
 __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uint32_t r, uint32_t Lw_rt, float sc,
                                            float bi, uint32_t K) {
   const uint32_t Lw = GUARD ? Lw_rt : 32u;   // stream (G == 1) tasks span the whole warp
@@ -498,7 +520,7 @@ __device__ __forceinline__ void decode_row(LaneRows& s, const uint8_t* ring, uin
   // the row's shift amounts and mask from the per-k table (one broadcast LDS.128, issued beside the
   // field's loads): dA = (d1 << 16) | d0 from field >> (16 - 2k) (d1 lands at bit 16) and
   // field >> (32 - k); dB the same from field << 2k
-  const uint4 T = ktab_entry(k);
+  const uint4 T = KT ? *reinterpret_cast<const uint4*>(ring + KT + 16u * k) : ktab_entry(k);
   const uint32_t g = shl_c(field, T.z);
   const uint32_t dA = ((shr_c(field, T.y) & T.w) | shr_c(field, T.x)) + base2;
   const uint32_t dB = ((shr_c(g, T.y) & T.w) | shr_c(g, T.x)) + base2;
@@ -617,19 +639,20 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
     stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
                    lane);
   s.raw = rbits(ring, s.bp);
-  decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, 0, Lw, sc, bi, K);
+  constexpr int KT = L3_KTAB_RING ? kKtabOff : 0;
+  decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
                      lane);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0>(s, ring, r, Lw, sc, bi, K);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1>(s, ring, r + 1, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1, KT>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
       stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
-    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED>(s, ring, r, Lw, sc, bi, K);
+    decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
   }
 }
 
@@ -676,8 +699,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
     fence_mbar_init();
   }
   if (L3_UNPACK_TAB) {
-    init_ktab();
-    __syncthreads();
+    if (L3_KTAB_RING) {   // this warp's copy, after its ring
+      if (lane < 16) {
+        const uint32_t k = (uint32_t)lane;
+        reinterpret_cast<uint4*>(ring + kKtabOff)[k] =
+            (k >= 1 && k <= 8) ? make_uint4(32u - k, 16u - 2u * k, 2u * k, ((1u << k) - 1u) << 16)
+                               : make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      init_ktab();
+      __syncthreads();
+    }
   }
   __syncwarp();
   uint32_t phase_bits = 0;
@@ -868,7 +900,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
       st.landed = 0;
       st.landed_end = 0;
       const uint32_t first = min(st.nchunks, (uint32_t)kSlots);
+#if L3_BULK_FIRST
+      // the first `first` chunks are contiguous in the ring: one bulk copy on bars[0]
+      if (first > 0) {   // (no arrive on bars[0] without a matching wait)
+        stage_range(p.pp.src, st.A, min(st.A + (uint64_t)first * kSlotBytes, st.B), lim, st.stage_end, ring,
+                    &bars[0], lane == 0, lane, 32);
+        st.issued = first;
+        st.group = first;
+      }
+#else
       while (st.issued < first) stream_issue(p.pp.src, lim, st, ring, bars, lane);
+#endif
       __syncwarp();
       s.bp = (uint32_t)(start - st.A) * 8u;
     }
@@ -920,9 +962,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
     }
     if (stream) {   // drain copies that were issued but never waited for
       while (st.landed < st.issued) {
-        const uint32_t sl = st.landed % kSlots;
-        mbar_wait(&bars[sl], (phase_bits >> sl) & 1u);
-        phase_bits ^= 1u << sl;
+        stream_land(st, bars, phase_bits);
         st.landed++;
       }
     }
