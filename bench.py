@@ -782,6 +782,11 @@ def run_throughput(args):
                       "~3 % of the step in the launch list)",
             "alg_bytes_per_launch": alg_bytes, "alg_bytes_formula": "compressed file bytes + decoded output bytes",
             "peak_source": peak_src}
+    ip = os.path.join(ROOT, "profiles", "ncu_instr.json")
+    if os.path.exists(ip):   # instruction efficiency of the same kernel (stored ncu count, like traffic)
+        ij = json.load(open(ip))
+        roof["warp_instr_per_sample"] = ij.get(f"{args.config}_{out_kind}")
+        roof["warp_instr_source"] = "stored: " + str(ij.get("source")) + " (profiles/ncu_instr.json)"
     if world > 1:   # sum of bytes / (max time x R x peak)
         roof["aggregate_frac"] = round(alg_bytes_all / (decode_ms_max / 1e3) / 1e9 / (world * peak), 4)
         roof["aggregate_alg_bytes"] = int(alg_bytes_all)

@@ -55,6 +55,11 @@ def kernel_md(path, samples):
     return "", None
 
 
+def _inst(path):
+    hdr, units, data = raw(path)
+    return float(dict(zip(hdr, data[0]))["smsp__inst_executed.sum"])
+
+
 def launches_md(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -84,6 +89,8 @@ if __name__ == "__main__":
     tag, gp = sys.argv[1], sys.argv[2]   # e.g. r1 gpurun_out/r1b
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
+    ij = os.path.join(ROOT, "profiles", "ncu_instr.json")
+    instr = json.load(open(ij)) if os.path.exists(ij) else {}
     sys.path.insert(0, ROOT)
     import l3synth
     c2 = sum(3 * h * w for h, w in l3synth.imagenet_shapes(256))
@@ -101,6 +108,8 @@ if __name__ == "__main__":
         lines = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_lines.py"), rep, "30"],
                                capture_output=True, text=True).stdout
         traffic[tkey] = t
+        instr[tkey] = \
+            round(_inst(rep) / samples, 4)
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{key}.md"), "w") as f:
             f.write(f"# {tag}: ncu --set full, decode kernel, {title}\n\n")
             f.write(f"Source: `{os.path.basename(rep)}` (one launch, `-s 3 -c 1`, --clock-control none).\n\n")
@@ -115,4 +124,6 @@ if __name__ == "__main__":
                     "`ncu --metrics gpu__time_duration.sum --clock-control none`\n\n")
             f.write(launches_md(lc) + "\n")
     json.dump(traffic, open(tj, "w"), indent=1)
+    instr["source"] = f"{tag}: smsp__inst_executed.sum / channel-samples of one launch (ncu --set full)"
+    json.dump(instr, open(ij, "w"), indent=1)
     print(json.dumps(traffic))
