@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
     s.kacc = 0;
     s.A = s.B = 0;
     s.Q = 0;
-    if (!F32 && L3_PRED4 != 0) {   // byte-form predictor: (left Q, Q) and (Q, right Q) selectors
+    if (!F32 && L3_PRED4 != 0 && L3_H2_U8 == 0) {   // byte-form predictor: (left Q, Q) and (Q, right Q) selectors
       s.selL = s.first ? 0x6544u : 0x6543u;
       s.selR = s.last ? 0x3321u : 0x4321u;
     } else {                         // L3_EDGE_SEL: TLA = prmt(left B, A, selL), TRB = prmt(B, right A, selR)
