@@ -20,6 +20,9 @@
 
 namespace l3 {
 
+#ifndef L3_ISSUE_REL
+#define L3_ISSUE_REL 1   // ring chunk issue with 32-bit A-relative bounds (the 64-bit form cost ~67 instr per chunk)
+#endif
 #ifndef L3_BULK_FIRST
 #define L3_BULK_FIRST 0   // planar streamed tasks: the first 8 KB of a unit as one bulk copy (measured slower)
 #endif
@@ -109,7 +112,39 @@ struct StreamState {
   uint32_t nchunks, issued, landed;
   uint32_t landed_end;  // A-relative bytes known to be resident (0xFFFFFFFF = all)
   uint32_t group = 0;   // chunks [0, group) were issued as ONE bulk copy on bars[0] (L3_BULK_FIRST)
+  // A-relative 32-bit bounds (stream_rel_init): B - A; the bytes a bulk copy may move (up to the batch end
+  // rounded down to 16); stage_end - A (the lanes copy [rel_bulk, rel_end) when the unit ends past it)
+  uint32_t relB, rel_bulk, rel_end;
 };
+
+template <class S>
+__device__ __forceinline__ void stream_rel_init(S& s, uint64_t lim) {
+  s.relB = (uint32_t)(s.B - s.A);
+  s.rel_bulk = lim > s.A ? (uint32_t)(min(s.B, lim) - s.A) : 0u;
+  s.rel_end = s.stage_end > s.A ? (uint32_t)(s.stage_end - s.A) : 0u;
+}
+
+// Issue chunk s.issued of [A, B) into its ring slot: one bulk copy by the leader lane (32-bit A-relative
+// bounds); only a unit ending past the batch's last 16-byte boundary has lane-copied tail bytes.
+template <int SLOTS, class S>
+__device__ __forceinline__ void stream_issue_rel(const uint8_t* src, S& s, uint8_t* ring, uint64_t* bars, bool leader,
+                                                 uint32_t lane, uint32_t lanes) {
+  const uint32_t c = s.issued;
+  const uint32_t ca = c * (uint32_t)kSlotBytes;
+  const uint32_t cb = min(ca + (uint32_t)kSlotBytes, s.relB);
+  const uint32_t be = min(cb, s.rel_bulk);
+  const uint32_t bulk = be > ca ? be - ca : 0u;
+  uint8_t* dst = ring + (c % SLOTS) * kSlotBytes;
+  if (leader) {
+    mbar_arrive_expect_tx(&bars[c % SLOTS], bulk);
+    if (bulk) bulk_g2s(dst, src + s.A + ca, bulk, &bars[c % SLOTS]);
+  }
+  if (s.rel_bulk < cb) {   // rare: the batch's last unit
+    const uint32_t te = min(cb, s.rel_end);
+    for (uint32_t x = max(ca, s.rel_bulk) + lane; x < te; x += lanes) dst[x - ca] = __ldg(src + s.A + x);
+  }
+  s.issued = c + 1;
+}
 
 // Wait for chunk s.landed (the first chunk of the initial group waits for the whole group).
 template <int SLOTS = kSlots>
@@ -124,9 +159,14 @@ __device__ __forceinline__ void stream_land(StreamState& s, uint64_t* bars, uint
   }
 }
 
-template <int SLOTS = kSlots>
+// REL: 32-bit A-relative bounds (the caller ran stream_rel_init), else the 64-bit stage_range form.
+template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0)>
 __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                              uint64_t* bars, int lane) {
+  if constexpr (REL) {
+    stream_issue_rel<SLOTS>(src, s, ring, bars, lane == 0, (uint32_t)lane, 32u);
+    return;
+  }
   const uint32_t c = s.issued;
   const uint64_t ca = s.A + (uint64_t)c * kSlotBytes;
   const uint64_t cb = min(ca + kSlotBytes, s.B);
@@ -137,7 +177,7 @@ __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, S
 
 // Slow path of the per-row ring test: refill consumed slots, then wait until
 // `need` A-relative bytes are resident. Warp-collective.
-template <int SLOTS = kSlots>
+template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0)>
 __device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                             uint64_t* bars, uint32_t& phase_bits, uint32_t consumed_byte,
                                             uint32_t need, int lane) {
@@ -145,7 +185,7 @@ __device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim,
   if (s.issued < s.nchunks && s.issued < consumed + SLOTS) {
     __syncwarp();
     fence_proxy_async_smem();
-    while (s.issued < s.nchunks && s.issued < consumed + SLOTS) stream_issue<SLOTS>(src, lim, s, ring, bars, lane);
+    while (s.issued < s.nchunks && s.issued < consumed + SLOTS) stream_issue<SLOTS, REL>(src, lim, s, ring, bars, lane);
     __syncwarp();
   }
   while (s.landed < s.issued && (uint64_t)s.landed * kSlotBytes < need) {
@@ -635,23 +675,25 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
                                                  StreamState& st, uint64_t* bars, uint32_t& phase_bits,
                                                  uint32_t rowmax, int lane) {
   constexpr bool GUARD = !STREAM;   // G == 1: every lane runs exactly the unit's h rows
+  // 32-bit chunk issue on the fp32 kernel only: the u8 narrow kernel measured slower with it (codegen)
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-    stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
-                   lane);
+    stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+                                                      (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD, lane);
   s.raw = rbits(ring, s.bp);
   constexpr int KT = L3_KTAB_RING ? kKtabOff : 0;
   decode_row<true, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, 0, Lw, sc, bi, K);
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD,
-                     lane);
+      stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+                                                        (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD, lane);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1, KT>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
-      stream_advance(src, lim, st, ring, bars, phase_bits, s.bp >> 3, (s.bp >> 3) + rowmax, lane);
+      stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+                                                        (s.bp >> 3) + rowmax, lane);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
   }
 }
@@ -895,6 +937,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
       st.A = start & ~15ull;
       st.B = (stage_end + 15) & ~15ull;
       st.stage_end = stage_end;
+      if (F32) stream_rel_init(st, lim);
       st.nchunks = active ? (uint32_t)((st.B - st.A + kSlotBytes - 1) / kSlotBytes) : 0u;
       st.issued = 0;
       st.landed = 0;
@@ -909,7 +952,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
         st.group = first;
       }
 #else
-      while (st.issued < first) stream_issue(p.pp.src, lim, st, ring, bars, lane);
+      while (st.issued < first) stream_issue<kSlots, F32 && L3_ISSUE_REL != 0>(p.pp.src, lim, st, ring, bars, lane);
 #endif
       __syncwarp();
       s.bp = (uint32_t)(start - st.A) * 8u;

@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
       st[c].A = start[c] & ~15ull;
       st[c].B = (stage_end + 15) & ~15ull;
       st[c].stage_end = stage_end;
+      stream_rel_init(st[c], lim);
       st[c].nchunks = act[c] ? (uint32_t)((st[c].B - st[c].A + kSlotBytes - 1) / kSlotBytes) : 0u;
       st[c].issued = 0;
       st[c].landed = 0;

@@ -50,17 +50,22 @@ __device__ __forceinline__ uint32_t shf_l_clamp(uint32_t lo, uint32_t hi, uint32
 struct Seg8 {
   uint64_t A, B, stage_end;
   uint32_t nchunks, issued, landed, landed_end;
+  uint32_t relB, rel_bulk, rel_end;   // A-relative bounds (stream_rel_init)
 };
 
 template <int SLOTS>
 __device__ __forceinline__ void w8_issue(const uint8_t* src, uint64_t lim, Seg8& s, uint8_t* ring, uint64_t* bars,
                                          uint32_t j, uint32_t L) {
+#if L3_ISSUE_REL
+  stream_issue_rel<SLOTS>(src, s, ring, bars, j == 0, j, L);
+#else
   const uint32_t c = s.issued;
   const uint64_t ca = s.A + (uint64_t)c * kSlotBytes;
   const uint64_t cb = min(ca + kSlotBytes, s.B);
   stage_range(src, ca, cb, lim, s.stage_end, ring + (c % SLOTS) * kSlotBytes, &bars[c % SLOTS], j == 0, (int)j,
               (int)L);
   s.issued = c + 1;
+#endif
 }
 
 // Refill consumed slots, then wait (and byte-swap) until `need` A-relative bytes
@@ -361,6 +366,7 @@ __device__ __forceinline__ uint32_t decode_task8(const DecodeParams& p, const Im
   st.A = start & ~15ull;
   st.B = (stage_end + 15) & ~15ull;
   st.stage_end = stage_end;
+  stream_rel_init(st, lim);
   st.nchunks = active ? (uint32_t)((st.B - st.A + kSlotBytes - 1) / kSlotBytes) : 0u;
   st.issued = 0;
   st.landed = 0;
