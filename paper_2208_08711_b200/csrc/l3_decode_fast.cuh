@@ -126,15 +126,15 @@ __device__ __forceinline__ void stream_rel_init(S& s, uint64_t lim) {
 
 // Issue chunk s.issued of [A, B) into its ring slot: one bulk copy by the leader lane (32-bit A-relative
 // bounds); only a unit ending past the batch's last 16-byte boundary has lane-copied tail bytes.
-template <int SLOTS, class S>
+template <int SLOTS, class S, int SB = kSlotBytes>
 __device__ __forceinline__ void stream_issue_rel(const uint8_t* src, S& s, uint8_t* ring, uint64_t* bars, bool leader,
                                                  uint32_t lane, uint32_t lanes) {
   const uint32_t c = s.issued;
-  const uint32_t ca = c * (uint32_t)kSlotBytes;
-  const uint32_t cb = min(ca + (uint32_t)kSlotBytes, s.relB);
+  const uint32_t ca = c * (uint32_t)SB;
+  const uint32_t cb = min(ca + (uint32_t)SB, s.relB);
   const uint32_t be = min(cb, s.rel_bulk);
   const uint32_t bulk = be > ca ? be - ca : 0u;
-  uint8_t* dst = ring + (c % SLOTS) * kSlotBytes;
+  uint8_t* dst = ring + (c % SLOTS) * SB;
   if (leader) {
     mbar_arrive_expect_tx(&bars[c % SLOTS], bulk);
     if (bulk) bulk_g2s(dst, src + s.A + ca, bulk, &bars[c % SLOTS]);
@@ -160,13 +160,15 @@ __device__ __forceinline__ void stream_land(StreamState& s, uint64_t* bars, uint
 }
 
 // REL: 32-bit A-relative bounds (the caller ran stream_rel_init), else the 64-bit stage_range form.
-template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0)>
+// SB: chunk (slot) bytes; the ring is SLOTS x SB bytes.
+template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0), int SB = kSlotBytes>
 __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                              uint64_t* bars, int lane) {
   if constexpr (REL) {
-    stream_issue_rel<SLOTS>(src, s, ring, bars, lane == 0, (uint32_t)lane, 32u);
+    stream_issue_rel<SLOTS, StreamState, SB>(src, s, ring, bars, lane == 0, (uint32_t)lane, 32u);
     return;
   }
+  static_assert(REL || SB == kSlotBytes, "64-bit issue: 1 KB chunks");
   const uint32_t c = s.issued;
   const uint64_t ca = s.A + (uint64_t)c * kSlotBytes;
   const uint64_t cb = min(ca + kSlotBytes, s.B);
@@ -177,32 +179,39 @@ __device__ __forceinline__ void stream_issue(const uint8_t* src, uint64_t lim, S
 
 // Slow path of the per-row ring test: refill consumed slots, then wait until
 // `need` A-relative bytes are resident. Warp-collective.
-template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0)>
+template <int SLOTS = kSlots, bool REL = (L3_ISSUE_REL != 0), int SB = kSlotBytes>
 __device__ __forceinline__ void stream_advance(const uint8_t* src, uint64_t lim, StreamState& s, uint8_t* ring,
                                             uint64_t* bars, uint32_t& phase_bits, uint32_t consumed_byte,
                                             uint32_t need, int lane) {
-  const uint32_t consumed = consumed_byte / kSlotBytes;
+  const uint32_t consumed = consumed_byte / SB;
   if (s.issued < s.nchunks && s.issued < consumed + SLOTS) {
     __syncwarp();
     fence_proxy_async_smem();
-    while (s.issued < s.nchunks && s.issued < consumed + SLOTS) stream_issue<SLOTS, REL>(src, lim, s, ring, bars, lane);
+    while (s.issued < s.nchunks && s.issued < consumed + SLOTS)
+      stream_issue<SLOTS, REL, SB>(src, lim, s, ring, bars, lane);
     __syncwarp();
   }
-  while (s.landed < s.issued && (uint64_t)s.landed * kSlotBytes < need) {
+  while (s.landed < s.issued && (uint64_t)s.landed * SB < need) {
     const uint32_t sl = s.landed % SLOTS;
     stream_land<SLOTS>(s, bars, phase_bits);
     __syncwarp();
-    swap_words(ring, sl * kSlotBytes, (sl + 1) * kSlotBytes, lane, 32);
+    swap_words(ring, sl * SB, (sl + 1) * SB, lane, 32);
     __syncwarp();
     if (sl == 0) {   // keep the 16-byte mirror of word 0.. after the ring end current
       if (lane < 4)
-        reinterpret_cast<uint32_t*>(ring + SLOTS * kSlotBytes)[lane] = reinterpret_cast<uint32_t*>(ring)[lane];
+        reinterpret_cast<uint32_t*>(ring + SLOTS * SB)[lane] = reinterpret_cast<uint32_t*>(ring)[lane];
       __syncwarp();
     }
     s.landed++;
   }
-  s.landed_end = (s.landed == s.nchunks) ? 0xFFFFFFFFu : s.landed * kSlotBytes;
+  s.landed_end = (s.landed == s.nchunks) ? 0xFFFFFFFFu : s.landed * SB;
 }
+
+#ifndef L3_STREAM_SB
+#define L3_STREAM_SB 1024   // fp32 planar streamed path: chunk bytes of the 8 KB ring (2048: 4 chunks)
+#endif
+template <bool F32> __host__ __device__ constexpr int kStreamSB() { return F32 ? L3_STREAM_SB : kSlotBytes; }
+template <bool F32> __host__ __device__ constexpr int kStreamSlots() { return kRingBytes / kStreamSB<F32>(); }
 
 // ---------------------------------------------------------------- SWAR core
 // Two samples per 32-bit register, one per 16-bit half (value in the half's
@@ -677,7 +686,7 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   constexpr bool GUARD = !STREAM;   // G == 1: every lane runs exactly the unit's h rows
   // 32-bit chunk issue on the fp32 kernel only: the u8 narrow kernel measured slower with it (codegen)
   if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-    stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+    stream_advance<kStreamSlots<F32>(), F32 && L3_ISSUE_REL != 0, kStreamSB<F32>()>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
                                                       (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD, lane);
   s.raw = rbits(ring, s.bp);
   constexpr int KT = L3_KTAB_RING ? kKtabOff : 0;
@@ -685,14 +694,14 @@ __device__ __forceinline__ void decode_unit_rows(LaneRows& s, uint8_t* ring, uin
   uint32_t r = 1;
   for (; r + 1 < hmax; r += 2) {   // two rows per ring test
     if (STREAM && (s.bp >> 3) + 2u * rowmax > st.landed_end)
-      stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+      stream_advance<kStreamSlots<F32>(), F32 && L3_ISSUE_REL != 0, kStreamSB<F32>()>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
                                                         (s.bp >> 3) + 2u * rowmax + L3_REFILL_AHEAD, lane);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 1, KT>(s, ring, r + 1, Lw, sc, bi, K);
   }
   if (r < hmax) {
     if (STREAM && (s.bp >> 3) + rowmax > st.landed_end)
-      stream_advance<kSlots, F32 && L3_ISSUE_REL != 0>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
+      stream_advance<kStreamSlots<F32>(), F32 && L3_ISSUE_REL != 0, kStreamSB<F32>()>(src, lim, st, ring, bars, phase_bits, s.bp >> 3,
                                                         (s.bp >> 3) + rowmax, lane);
     decode_row<false, F32, FAST, GUARD, CROP, true, kSlots, HWC, RAGGED, 0, KT>(s, ring, r, Lw, sc, bi, K);
   }
@@ -938,21 +947,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
       st.B = (stage_end + 15) & ~15ull;
       st.stage_end = stage_end;
       if (F32) stream_rel_init(st, lim);
-      st.nchunks = active ? (uint32_t)((st.B - st.A + kSlotBytes - 1) / kSlotBytes) : 0u;
+      constexpr int SB = kStreamSB<F32>(), SS = kStreamSlots<F32>();
+      st.nchunks = active ? (uint32_t)((st.B - st.A + SB - 1) / SB) : 0u;
       st.issued = 0;
       st.landed = 0;
       st.landed_end = 0;
-      const uint32_t first = min(st.nchunks, (uint32_t)kSlots);
+      const uint32_t first = min(st.nchunks, (uint32_t)SS);
 #if L3_BULK_FIRST
       // the first `first` chunks are contiguous in the ring: one bulk copy on bars[0]
       if (first > 0) {   // (no arrive on bars[0] without a matching wait)
-        stage_range(p.pp.src, st.A, min(st.A + (uint64_t)first * kSlotBytes, st.B), lim, st.stage_end, ring,
+        stage_range(p.pp.src, st.A, min(st.A + (uint64_t)first * SB, st.B), lim, st.stage_end, ring,
                     &bars[0], lane == 0, lane, 32);
         st.issued = first;
         st.group = first;
       }
 #else
-      while (st.issued < first) stream_issue<kSlots, F32 && L3_ISSUE_REL != 0>(p.pp.src, lim, st, ring, bars, lane);
+      while (st.issued < first) stream_issue<SS, F32 && L3_ISSUE_REL != 0, SB>(p.pp.src, lim, st, ring, bars, lane);
 #endif
       __syncwarp();
       s.bp = (uint32_t)(start - st.A) * 8u;
@@ -1005,7 +1015,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
     }
     if (stream) {   // drain copies that were issued but never waited for
       while (st.landed < st.issued) {
-        stream_land(st, bars, phase_bits);
+        stream_land<kStreamSlots<F32>()>(st, bars, phase_bits);
         st.landed++;
       }
     }
