@@ -21,7 +21,11 @@ constexpr int kHwcWarps = 2;
 #define L3_HWC_SLOTS 4
 #endif
 constexpr int kHwcSlots = L3_HWC_SLOTS;                       // 4 KB ring per channel stream
-constexpr int kHwcPitch = kHwcSlots * kSlotBytes + 64;        // + wrap mirror
+#ifndef L3_HWC_KTAB
+#define L3_HWC_KTAB 1   // streamed tiles: a copy of the per-k unpack table after each channel ring (KT)
+#endif
+constexpr int kHwcKtab = kHwcSlots * kSlotBytes + 64;        // the table's offset in a channel ring region
+constexpr int kHwcPitch = kHwcSlots * kSlotBytes + 64 + (L3_HWC_KTAB ? 256 : 0);   // + wrap mirror + table
 // 3 rings per warp: 2 warps = 25 KB per CTA; the register file then bounds residency (16 warps / SM)
 __host__ __device__ constexpr size_t hwc_smem_bytes() {
   return (size_t)kHwcWarps * 3 * kHwcPitch + (size_t)kHwcWarps * 3 * kHwcSlots * 8 + 16;
@@ -199,6 +203,9 @@ __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint6
   constexpr bool FAST = MODE != kStRagged && MODE != kStWindow;   // window tiles may be ragged: ghost columns
   constexpr bool GUARD = !STREAM;
   constexpr int SLOTS = STREAM ? kHwcSlots : 16;   // whole-staged: one linear 12 KB buffer, no wrap
+  // streamed: the unpack table copy after each channel ring (rewritten per tile: whole-staged tasks may
+  // have staged over it); whole-staged: the static table
+  constexpr int KT = (STREAM && L3_HWC_KTAB) ? kHwcKtab : 0;
   constexpr uint32_t rowmax = (12u + 8u * 128u) / 8u + 10u;
 #pragma unroll
   for (int c = 0; c < 3; c++) {
@@ -210,8 +217,8 @@ __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint6
   }
 #pragma unroll
   for (int c = 0; c < 3; c++)
-    decode_row<true, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, 0, Lw,
-                                                              0.f, 0.f, K);
+    decode_row<true, false, FAST, GUARD, false, false, SLOTS, false, !FAST, 0, KT>(
+        s[c], STREAM ? rings + c * kHwcPitch : rings, 0, Lw, 0.f, 0.f, K);
   if (MODE == kStWindow) store12w<F32>(optr, s[0], s[1], s[2], sc, bi, s[0].h > 0, wr);
   else store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && s[0].h > 0);
   optr += pitch;
@@ -227,8 +234,8 @@ __device__ __forceinline__ void hwc_tile_rows(LaneRows* s, uint8_t* rings, uint6
     }
 #pragma unroll
     for (int c = 0; c < 3; c++)
-      decode_row<false, false, FAST, GUARD, false, false, SLOTS>(s[c], STREAM ? rings + c * kHwcPitch : rings, r,
-                                                                 Lw, 0.f, 0.f, K);
+      decode_row<false, false, FAST, GUARD, false, false, SLOTS, false, !FAST, 0, KT>(
+          s[c], STREAM ? rings + c * kHwcPitch : rings, r, Lw, 0.f, 0.f, K);
     if (MODE == kStWindow) store12w<F32>(optr, s[0], s[1], s[2], sc, bi, r < s[0].h, wr);
     else store12<F32, MODE>(optr, s[0], s[1], s[2], sc, bi, valid && r < s[0].h);
     optr += pitch;
@@ -510,6 +517,13 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
         stream_issue<kHwcSlots>(p.pp.src, lim, st[c], rings + c * kHwcPitch, bars + c * kHwcSlots, lane);
       s[c].bp = act[c] ? (uint32_t)(start[c] - st[c].A) * 8u : 0u;
       s[c].lim = s[c].bp + len * 8u;
+    }
+    if (L3_HWC_KTAB && lane < 16) {   // the unpack table after each channel ring (see hwc_tile_rows)
+      const uint32_t k = (uint32_t)lane;
+      const uint4 e = (k >= 1 && k <= 8) ? make_uint4(32u - k, 16u - 2u * k, 2u * k, ((1u << k) - 1u) << 16)
+                                         : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int c = 0; c < 3; c++) reinterpret_cast<uint4*>(rings + c * kHwcPitch + kHwcKtab)[k] = e;
     }
     __syncwarp();
 
