@@ -178,7 +178,6 @@ __device__ __forceinline__ void parse_phase_simple(const ParseParams& p, uint64_
         d.tasks = 0;
       }
       p.ws.desc[i] = d;
-      p.ws.errkey[i] = kNoError;
       p.status[i] = st;
       if (p.bad_unit) p.bad_unit[i] = -1;
     }
@@ -249,7 +248,6 @@ __device__ void parse_phase(const ParseParams& p, uint64_t* sh_a, uint64_t* sh_b
         d.tasks = 0;
       }
       p.ws.desc[i] = d;
-      p.ws.errkey[i] = kNoError;
       p.status[i] = st;
       if (p.bad_unit) p.bad_unit[i] = -1;
     }
@@ -302,6 +300,7 @@ struct DecodeParams {
   void* out;
   float scale[3], bias[3];
   uint32_t key_scale;       // 128: predictor key scale, passed at run time (keeps key math on IMAD)
+  uint32_t a1in;            // planar kernels: a1 inside every decode CTA into shared memory (n <= kA1InMaxN)
 };
 
 __device__ __forceinline__ uint32_t err_key(uint32_t unit, int code) {
@@ -344,6 +343,8 @@ struct GenericArgs {
   const uint8_t* src;
   const uint64_t* prefix1;
   const ImgDesc* desc;
+  const uint32_t* a1_pre1;    // a1 inside the decode CTA: its shared class-1 prefix and compact descriptors
+  const A1Compact* a1_desc;   // (else NULL: the workspace's)
   uint32_t* errkey;
   void* out;
   uint64_t lim;
@@ -362,11 +363,11 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
   int lo = 0, hi = ga.n;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (__ldcg(&prefix[mid]) <= task) lo = mid; else hi = mid;
+    if ((ga.a1_desc ? (uint64_t)ga.a1_pre1[mid] : __ldcg(&prefix[mid])) <= task) lo = mid; else hi = mid;
   }
   const int img = lo;
-  const ImgDesc d = ga.desc[img];
-  const uint32_t u = (uint32_t)(task - prefix[img]);   // G = 1: task = unit
+  const ImgDesc d = ga.a1_desc ? a1_expand(ga.a1_desc[img]) : ga.desc[img];
+  const uint32_t u = (uint32_t)(task - (ga.a1_desc ? (uint64_t)ga.a1_pre1[img] : prefix[img]));   // G = 1: task = unit
   const uint32_t j = lane;
   const uint32_t nunits = 3u * d.P;
   const uint8_t* file = ga.src + d.file_off;
@@ -383,7 +384,7 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
   const uint64_t off = ld_u32le(file + 13 + 4ull * u);
   const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
   if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
-    if (lane == 0) atomicMin(&ga.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+    if (lane == 0) record_err(&ga.errkey[img], 0u);   // header-level: CORRUPT_HEADER
     return phase_bits;
   }
   const uint64_t start = d.data_off + off, end = d.data_off + nxt;
@@ -437,7 +438,7 @@ __device__ __noinline__ uint32_t generic_task(GenericArgs ga, uint64_t task, uin
       else if (k == 0 || k > 8) code = L3_E_CORRUPT_STREAM;
       else if (avail < 12u + k * w) code = L3_E_TRUNCATED_STREAM;
       if (code != L3_OK) {
-        if (lane == 0) atomicMin(&ga.errkey[img], err_key(u, code));
+        if (lane == 0) record_err(&ga.errkey[img], err_key(u, code));
         dead = true;
         live = false;
         k = 1;
@@ -738,8 +739,13 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   if (a->max_ctas > 0 && (int)a->max_ctas < grid) grid = (int)a->max_ctas;
   dp.pp.tail_units = (uint32_t)grid * kWarpsPerCta;   // about one tail patch per resident warp
   dp.pp.wide = wide ? 1u : 0u;
+  // small planar batches: a1 inside every decode CTA, CTA-local (one launch; the a1 launch and its PDL
+  // hand-off cost ~6.5 us per call, scripts/exp_skip_prep.py); larger batches keep the one-block a1 kernel
+  static const int a1in_max = getenv("L3_A1IN_MAX") ? atoi(getenv("L3_A1IN_MAX")) : kA1InMaxN;
+  dp.a1in = (!tile && !crop && !wide && a->n <= min(a1in_max, kA1InMaxN)) ? 1u : 0u;
   // launch 1: a1 (one CTA); launch 2: the persistent decode grid, programmatically dependent on it
-  if (tile) l3_prep_kernel<false, true, true><<<1, kPrepThreads, 0, s>>>(dp.pp);
+  if (dp.a1in) {
+  } else if (tile) l3_prep_kernel<false, true, true><<<1, kPrepThreads, 0, s>>>(dp.pp);
   else if (wide) l3_prep_kernel<true, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
   else l3_prep_kernel<false, false, false><<<1, kPrepThreads, 0, s>>>(dp.pp);
   e = cudaGetLastError();
@@ -751,7 +757,7 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   cfg.gridDim = dim3(grid);
   cfg.stream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = dp.a1in ? 0 : 1;   // a1 inside the grid: plain stream order
   if (tile) {
     cfg.blockDim = dim3(kHwcWarps * 32);
     cfg.dynamicSmemBytes = hwc_smem_bytes();

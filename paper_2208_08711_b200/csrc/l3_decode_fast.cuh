@@ -46,7 +46,10 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
 // key 0 = header-level error, else 1<<31 | unit<<1 | truncated) into status / bad_unit, the
 // result of a sequential decode, and re-zeroes the workspace head so
 // the next launch on this workspace needs no host work.
-__device__ __forceinline__ void a7_finish(const ParseParams& pp, WsHead* head, unsigned int* sh_ticket) {
+// A1: a1 ran inside the CTAs (a1_desc: this CTA's shared results, with each image's header status);
+// the finisher then writes every image's status and bad_unit.
+__device__ __forceinline__ void a7_finish(const ParseParams& pp, WsHead* head, unsigned int* sh_ticket,
+                                          const A1Compact* a1_desc = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -56,11 +59,17 @@ __device__ __forceinline__ void a7_finish(const ParseParams& pp, WsHead* head, u
   if (*sh_ticket != gridDim.x - 1) return;
   __threadfence();
   for (int i = threadIdx.x; i < pp.n; i += blockDim.x) {
-    if (pp.status[i] != L3_OK) continue;   // header-level error from a1
-    const uint32_t key = atomicAdd(&pp.ws.errkey[i], 0u);
+    const uint32_t key = ~atomicExch(&pp.ws.errkey[i], 0u);   // read and re-zero (record_err encoding)
+    const int32_t st = a1_desc ? a1_desc[i].st : pp.status[i];
+    if (a1_desc && (st != L3_OK || key == kNoError)) {
+      pp.status[i] = st;
+      if (pp.bad_unit) pp.bad_unit[i] = -1;
+    }
+    if (st != L3_OK) continue;   // header-level error from a1
     if (key == kNoError) continue;
     if (key == 0u) {
       pp.status[i] = L3_E_CORRUPT_HEADER;
+      if (a1_desc && pp.bad_unit) pp.bad_unit[i] = -1;
     } else {
       pp.status[i] = (key & 1u) ? L3_E_TRUNCATED_STREAM : L3_E_CORRUPT_STREAM;
       if (pp.bad_unit) pp.bad_unit[i] = (int32_t)((key >> 1) & 0x3FFFFFFFu);
@@ -737,6 +746,58 @@ namespace l3 {
 // small patches); WIDE (u8 out, L3_DECODE_HINT_WIDE) carries the 8-column path
 // for 33 <= N <= 128 and runs at 4 CTAs per SM.
 // HWC (with CROP only): the augment variant writes the window interleaved [h, w, 3].
+// a1 inside a decode CTA (n <= kA1InMaxN = 32, warp 0): the same header parse and decomposition as
+// l3_prep_kernel's, kept in this CTA's shared memory: compact descriptors and the
+// exclusive task prefixes of the two classes (N <= 128, N > 128), totals at [n].
+__device__ __forceinline__ void a1_in_cta(const ParseParams& pp, int lane, uint32_t* pre0, uint32_t* pre1,
+                                          A1Compact* a1d) {
+  uint32_t t0 = 0, t1 = 0;
+  if (lane < pp.n) {
+    ImgDesc d;
+    const int st = parse_header<false, false>(pp, lane, d);
+    A1Compact c = {};
+    c.st = st;
+    if (st == L3_OK) {
+      if (d.mode == 1 || d.mode == 2) {   // the narrow kernels: every 33 <= N <= 128 unit is a 1-patch task
+        d.mode = 4;
+        d.L = 32;
+        d.G = 1;
+      }
+      const uint32_t tasks = (uint32_t)((3ull * d.P + d.G - 1) / d.G);
+      if (d.mode != 3) t0 = tasks; else t1 = tasks;
+      c.file_off = d.file_off;
+      c.out_off = d.out_off;
+      c.data_len = d.data_len;
+      c.W = d.W;
+      c.H = d.H;
+      c.gx = d.gx;
+      c.P = d.P;
+      c.N = (uint8_t)d.N;
+      c.mode = (uint8_t)d.mode;
+      c.G = (uint8_t)d.G;
+      c.L = (uint8_t)d.L;
+    }
+    a1d[lane] = c;
+  }
+  uint32_t i0 = t0, i1 = t1;   // inclusive scans over the warp (lanes >= n add 0)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v0 = __shfl_up_sync(0xffffffffu, i0, o), v1 = __shfl_up_sync(0xffffffffu, i1, o);
+    if (lane >= o) {
+      i0 += v0;
+      i1 += v1;
+    }
+  }
+  if (lane < pp.n) {
+    pre0[lane] = i0 - t0;
+    pre1[lane] = i1 - t1;
+  }
+  if (lane == 31) {
+    pre0[pp.n] = i0;
+    pre1[pp.n] = i1;
+  }
+}
+
 template <bool F32, bool WIDE, bool CROP, bool HWC = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_MIN_CTAS : L3_MIN_CTAS))
     l3_decode_kernel(DecodeParams p) {
@@ -766,20 +827,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   uint32_t phase_bits = 0;
   WsHead* head = p.pp.ws.head;
 
-  // ---- a1 ran in the preceding l3_prep_kernel (PDL): wait until its results are visible
-  pdl_wait();
+  // shared prefix copy (large batches) or the a1-in-CTA results (small batches): pre0 [34], pre1 [34]
+  // u32, then 32 compact descriptors at byte 272 (1808 of the 2056 bytes)
+  __shared__ uint64_t sh_prefix[kShPrefix + 1];
+  uint32_t* const a1_pre0 = reinterpret_cast<uint32_t*>(sh_prefix);
+  uint32_t* const a1_pre1 = a1_pre0 + 34;
+  A1Compact* const a1_desc = reinterpret_cast<A1Compact*>(sh_prefix + 34);
+  const bool a1in = !CROP && !WIDE && p.a1in != 0;
+  if (a1in) {   // a1 inside this CTA (launch_decode_batch: n <= kA1InMaxN, no a1 launch)
+    if (warp == 0) a1_in_cta(p.pp, lane, a1_pre0, a1_pre1, a1_desc);
+    __syncthreads();
+  } else {
+    // ---- a1 ran in the preceding l3_prep_kernel (PDL): wait until its results are visible
+    pdl_wait();
+  }
 
   const uint64_t* prefix = p.pp.ws.prefix[0];
 #if L3_SMEM_PREFIX
   // task -> image lookup from a shared-memory copy of the task prefix (batches of <= 256 images)
-  __shared__ uint64_t sh_prefix[kShPrefix + 1];
-  const bool pref_smem = p.pp.n <= kShPrefix;
+  const bool pref_smem = !a1in && p.pp.n <= kShPrefix;
   if (pref_smem) {
     for (int i = threadIdx.x; i <= p.pp.n; i += blockDim.x) sh_prefix[i] = __ldcg(&prefix[i]);
     __syncthreads();
   }
 #endif
-  const uint64_t total_tasks = prefix[p.pp.n];
+  const uint64_t total_tasks = a1in ? (uint64_t)a1_pre0[p.pp.n] : prefix[p.pp.n];
   const uint64_t lim = p.pp.src_offsets[p.pp.n] & ~15ull;
   const uint32_t K = p.key_scale;
 
@@ -789,6 +861,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   uint64_t task = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
   while (task < total_tasks) {
     int lo = 0, hi = p.pp.n;
+    if (a1in) {
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a1_pre0[mid] <= task) lo = mid; else hi = mid;
+      }
+    } else
 #if L3_SMEM_PREFIX
     if (pref_smem) {
       while (hi - lo > 1) {
@@ -802,8 +880,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
       if (__ldcg(&prefix[mid]) <= task) lo = mid; else hi = mid;
     }
     const int img = lo;
-    const ImgDesc d = p.pp.ws.desc[img];
-    const uint32_t t = (uint32_t)(task - prefix[img]);
+    const ImgDesc d = a1in ? a1_expand(a1_desc[img]) : p.pp.ws.desc[img];
+    const uint32_t t = (uint32_t)(task - (a1in ? (uint64_t)a1_pre0[img] : prefix[img]));
     // claim the next task now; the atomic's latency hides behind this one
     uint64_t next = 0;
     if (lane == 0) next = grid_warps + atomicAdd(&head->next_task[0], 1ull);
@@ -856,7 +934,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
       if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
-        if (j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+        if (j == 0) record_err(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
         active = false;
       } else {
         start = d.data_off + off;
@@ -1011,7 +1089,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
     const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
     if (__any_sync(0xffffffffu, err) && err && j == 0) {   // a7: exact first error of a failed unit
       const int code = unit_first_error(p.pp.src, start, end, w, h);
-      if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key(u, code));
+      if (code != L3_OK) record_err(&p.pp.ws.errkey[img], err_key(u, code));
     }
     if (stream) {   // drain copies that were issued but never waited for
       while (st.landed < st.issued) {
@@ -1025,12 +1103,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   }
 
   // ---- N > 128 units (never chosen by the policy): generic path, same ring
-  const uint64_t total1 = p.pp.ws.prefix[1][p.pp.n];
+  const uint64_t total1 = a1in ? (uint64_t)a1_pre1[p.pp.n] : p.pp.ws.prefix[1][p.pp.n];
   if (total1 > 0) {
     GenericArgs ga;
     ga.src = p.pp.src;
     ga.prefix1 = p.pp.ws.prefix[1];
     ga.desc = p.pp.ws.desc;
+    ga.a1_pre1 = a1in ? a1_pre1 : nullptr;
+    ga.a1_desc = a1in ? a1_desc : nullptr;
     ga.errkey = p.pp.ws.errkey;
     ga.out = p.out;
     ga.lim = lim;
@@ -1049,7 +1129,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   }
 
   // ---- a7: per-image status, by the last CTA
-  a7_finish(p.pp, head, &ticket);
+  a7_finish(p.pp, head, &ticket, a1in ? a1_desc : nullptr);
 }
 
 }  // namespace l3

@@ -305,7 +305,7 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
       nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
     }
     act[c] = tact && !(unit_offsets_bad(u, nunits, off, nxt, d.data_len));
-    if (tact && !act[c] && j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+    if (tact && !act[c] && j == 0) record_err(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
     start[c] = act[c] ? d.data_off + off : 0;
     end[c] = act[c] ? d.data_off + nxt : 0;
     sEnd[c] = act[c] ? min(end[c], start[c] + worst + 8) : 0;
@@ -414,7 +414,7 @@ __device__ __forceinline__ uint32_t hwc_small_task(const DecodeParams& p, const 
       const bool err = mine && act[c] && (s[c].kacc >= 0x80000000u || s[c].bp > s[c].lim);
       if (err && j == 0) {   // a7: exact first error of a failed unit
         const int code = unit_first_error(p.pp.src, start[c], end[c], w, h);
-        if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
+        if (code != L3_OK) record_err(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
       }
     }
     __syncwarp();
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
       const uint64_t off = ld_u32le(file + 13 + 4ull * u);
       const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
       act[c] = !(unit_offsets_bad(u, nunits, off, nxt, d.data_len));
-      if (!act[c] && lane == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+      if (!act[c] && lane == 0) record_err(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
       start[c] = act[c] ? d.data_off + off : 0;
       end[c] = act[c] ? d.data_off + nxt : 0;
       const uint64_t stage_end = act[c] ? min(end[c], start[c] + worst + 8) : 0;
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
       const bool err = act[c] && (s[c].kacc >= 0x80000000u || s[c].bp > s[c].lim);
       if (err && lane == 0) {   // a7: exact first error of a failed unit
         const int code = unit_first_error(p.pp.src, start[c], end[c], w, h);
-        if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
+        if (code != L3_OK) record_err(&p.pp.ws.errkey[img], err_key((uint32_t)c * d.P + tile, code));
       }
       while (st[c].landed < st[c].issued) {   // drain copies that were issued but never waited for
         const uint32_t sl = st[c].landed % kHwcSlots;
@@ -579,6 +579,8 @@ __global__ void __launch_bounds__(kHwcWarps * 32, L3_HWC_MIN_CTAS) l3_decode_hwc
     ga.src = p.pp.src;
     ga.prefix1 = p.pp.ws.prefix[1];
     ga.desc = p.pp.ws.desc;
+    ga.a1_pre1 = nullptr;
+    ga.a1_desc = nullptr;
     ga.errkey = p.pp.ws.errkey;
     ga.out = p.out;
     ga.lim = lim;

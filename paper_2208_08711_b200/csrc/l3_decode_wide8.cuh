@@ -351,7 +351,7 @@ __device__ __forceinline__ uint32_t decode_task8(const DecodeParams& p, const Im
     const uint64_t off = ld_u32le(file + 13 + 4ull * u);
     const uint64_t nxt = (u + 1 < nunits) ? (uint64_t)ld_u32le(file + 17 + 4ull * u) : d.data_len;
     if (unit_offsets_bad(u, nunits, off, nxt, d.data_len)) {
-      if (j == 0) atomicMin(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
+      if (j == 0) record_err(&p.pp.ws.errkey[img], 0u);   // header-level: CORRUPT_HEADER
       active = false;
     } else {
       start = d.data_off + off;
@@ -418,7 +418,7 @@ __device__ __forceinline__ uint32_t decode_task8(const DecodeParams& p, const Im
   const bool err = active && (s.kacc >= 0x80000000u || s.bp > s.lim);
   if (__any_sync(0xffffffffu, err) && err && j == 0) {   // a7: exact first error of a failed unit
     const int code = unit_first_error(p.pp.src, start, end, w, h);
-    if (code != L3_OK) atomicMin(&p.pp.ws.errkey[img], err_key(u, code));
+    if (code != L3_OK) record_err(&p.pp.ws.errkey[img], err_key(u, code));
   }
   // drain copies that were issued but never waited for
   while (st.landed < st.issued) {

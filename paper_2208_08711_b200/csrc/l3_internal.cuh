@@ -99,6 +99,38 @@ __host__ __device__ inline void lanes_and_group(uint32_t N, uint32_t* L, uint32_
   *mode = 0;
 }
 
+// Per-image first-error key, stored complemented so that 0 means "no error": a zero-filled workspace is
+// clean with no launch-time initialisation (a1 may run inside the decode CTAs), and the a7 finisher
+// re-zeroes each key after reading it. record_err keeps the minimum key (atomicMax of ~key).
+__device__ __forceinline__ void record_err(uint32_t* slot, uint32_t key) { atomicMax(slot, ~key); }
+
+// a1 results kept in a decode CTA's shared memory (small batches, no a1 launch): the fields of ImgDesc the
+// planar kernels use; data_off is file_off + 13 + 12 P.
+struct A1Compact {
+  uint64_t file_off, out_off, data_len;
+  uint32_t W, H, gx, P;
+  uint8_t N, mode, G, L;
+  int32_t st;   // header status of a1 (L3_OK or the error)
+};
+static_assert(sizeof(A1Compact) == 48, "A1Compact");
+constexpr int kA1InMaxN = 32;   // batches of up to this many images run a1 inside every decode CTA
+__device__ __forceinline__ ImgDesc a1_expand(const A1Compact& c) {
+  ImgDesc d = ImgDesc{};
+  d.file_off = c.file_off;
+  d.data_off = c.file_off + 13ull + 12ull * c.P;
+  d.data_len = c.data_len;
+  d.out_off = c.out_off;
+  d.W = c.W;
+  d.H = c.H;
+  d.N = c.N;
+  d.gx = c.gx;
+  d.P = c.P;
+  d.G = c.G;
+  d.L = c.L;
+  d.mode = c.mode;
+  return d;
+}
+
 // Per-unit half of the a1 offset-table check (the oracle's
 // header rule): offsets start at 0, strictly increase over R||G||B and stay inside the data
 // section. Unit u checks its own offset and the next one, so a file truncated inside unit u's
