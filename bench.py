@@ -509,7 +509,7 @@ def run_latency(args):
                     "d2h_bytes_per_step": 4,
                     "call": "l3_load_decode_batch (pinned host src -> HBM, decode, status -> pinned host) + "
                             "stream synchronise, wall clock per call"},
-            "gpu_launches": args.steps * l3.l3_decode_kernels_per_call(),
+            "gpu_launches": args.steps * l3.l3_decode_launches(a),
             "clocks": sampler.summary(), "status_ok": True, "self_check": True}
     print(json.dumps(line), flush=True)
 
@@ -853,7 +853,7 @@ def run_throughput(args):
                             "decode",
                     "h2d_gbs_measured": round(h2d_gbs, 2), "e2e_compressed_gbs": round(e2e_gbs, 2),
                     "frac_of_h2d": round(e2e_gbs / h2d_gbs, 4)},
-            "gpu_launches": args.steps * l3.l3_decode_kernels_per_call(),
+            "gpu_launches": args.steps * l3.l3_decode_launches(args_list[0]),
             "clocks": clocks,
             "status_ok": status_ok, "self_check": ok,
         }

@@ -8,6 +8,7 @@
 namespace l3 {
 cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_variant = false);
 cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s);
+bool a1_in_cta_call(const l3_decode_args* a);
 cudaError_t launch_selftest_paeth(uint8_t* out, cudaStream_t s);
 cudaError_t launch_selftest_paeth4(uint8_t* out, cudaStream_t s);
 cudaError_t launch_selftest_paeth_h2(uint8_t* out, cudaStream_t s);
@@ -33,6 +34,12 @@ extern "C" {
 uint64_t l3_decode_workspace_size(int32_t n) { return n < 0 ? 0 : l3::WsView::bytes(n); }
 
 int32_t l3_decode_kernels_per_call(void) { return 2; }
+
+int32_t l3_decode_launches(const l3_decode_args* a) {
+  if (check_decode_args(a) != L3_OK) return -1;
+  if (a->n == 0) return 0;
+  return l3::a1_in_cta_call(a) ? 1 : 2;
+}
 
 l3_status_t l3_parse_batch(const l3_decode_args* a, l3_stream_t stream) {
   l3_status_t st = check_decode_args(a);

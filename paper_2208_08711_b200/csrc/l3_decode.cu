@@ -706,6 +706,17 @@ cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_va
   return cudaGetLastError();
 }
 
+// Does this call run a1 inside the decode CTAs (one launch) rather than as its own one-block launch?
+// Planar (not crop, not HWC), narrow (u8 without the wide hint, or fp32) batches of <= kA1InMaxN images.
+bool a1_in_cta_call(const l3_decode_args* a) {
+  static const int a1in_max = getenv("L3_A1IN_MAX") ? atoi(getenv("L3_A1IN_MAX")) : kA1InMaxN;   // dev A/B
+  const bool f32 = a->out_kind == L3_OUT_F32;
+  const bool crop = a->crops != nullptr;
+  const bool hwc = (a->flags & L3_DECODE_LAYOUT_HWC) != 0;
+  const bool wide = !crop && !f32 && (a->flags & L3_DECODE_HINT_WIDE);
+  return !hwc && !crop && !wide && a->n <= min(a1in_max, kA1InMaxN);
+}
+
 // The whole hot path in ONE persistent launch (grid = SMs x resident CTAs, or fewer CTAs when the
 // caller caps the decoder's share of the GPU with max_ctas, l3.h).
 cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
@@ -741,8 +752,7 @@ cudaError_t launch_decode_batch(const l3_decode_args* a, cudaStream_t s) {
   dp.pp.wide = wide ? 1u : 0u;
   // small planar batches: a1 inside every decode CTA, CTA-local (one launch; the a1 launch and its PDL
   // hand-off cost ~6.5 us per call, scripts/exp_skip_prep.py); larger batches keep the one-block a1 kernel
-  static const int a1in_max = getenv("L3_A1IN_MAX") ? atoi(getenv("L3_A1IN_MAX")) : kA1InMaxN;
-  dp.a1in = (!tile && !crop && !wide && a->n <= min(a1in_max, kA1InMaxN)) ? 1u : 0u;
+  dp.a1in = a1_in_cta_call(a) ? 1u : 0u;
   // launch 1: a1 (one CTA); launch 2: the persistent decode grid, programmatically dependent on it
   if (dp.a1in) {
   } else if (tile) l3_prep_kernel<false, true, true><<<1, kPrepThreads, 0, s>>>(dp.pp);

@@ -99,6 +99,8 @@ def lib() -> ctypes.CDLL:
             L.l3_decode_workspace_size.restype = ctypes.c_uint64
             L.l3_decode_kernels_per_call.argtypes = []
             L.l3_decode_kernels_per_call.restype = ctypes.c_int32
+            L.l3_decode_launches.argtypes = [ctypes.c_void_p]
+            L.l3_decode_launches.restype = ctypes.c_int32
             L.l3_decode_batch_ablation.argtypes = [P(l3_decode_args), ctypes.c_int32, ctypes.c_void_p]
             L.l3_decode_batch_ablation.restype = ctypes.c_int
             L.l3_selftest_paeth.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
@@ -122,7 +124,8 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("l3_decode_workspace_size", "l3_decode_batch", "l3_parse_batch",
-            "l3_load_decode_batch", "l3_decode_kernels_per_call", "l3_status_string", "l3_choose_patch_size",
+            "l3_load_decode_batch", "l3_decode_kernels_per_call", "l3_decode_launches", "l3_status_string",
+            "l3_choose_patch_size",
             "l3_encode_max_bytes", "l3_encode_workspace_size", "l3_encode_batch", "l3_selftest_paeth",
             "l3_selftest_paeth4", "l3_selftest_paeth_h2", "l3_decode_batch_ablation")
 
@@ -184,6 +187,10 @@ def l3_decode_workspace_size(n: int) -> int:
 
 def l3_decode_kernels_per_call() -> int:
     return int(lib().l3_decode_kernels_per_call())
+
+
+def l3_decode_launches(args: l3_decode_args) -> int:
+    return int(lib().l3_decode_launches(ctypes.byref(args)))
 
 
 def l3_decode_batch(args: l3_decode_args, stream=None) -> None:

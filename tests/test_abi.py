@@ -66,6 +66,26 @@ def test_host_helpers(lib):
     assert l3.l3_status_string(4) == "corrupt stream"
     assert l3.l3_decode_workspace_size(32) >= 32 * 64
     assert l3.l3_decode_kernels_per_call() == 2
+    # launches of a given call (host-only, no pointer is dereferenced): a1 inside the decode grid for
+    # planar batches of <= 32 images, else the a1 kernel + the decode grid
+    from paper_2208_08711_b200.l3 import L3_DECODE_HINT_WIDE, L3_DECODE_LAYOUT_HWC, l3_decode_args
+    a = l3_decode_args()
+    assert l3.l3_decode_launches(a) == 0   # empty batch: no launch
+    a.n = 1
+    assert l3.l3_decode_launches(a) == -1   # NULL pointers: invalid, like l3_decode_batch
+    a.src = a.src_offsets = a.shapes = a.out = a.status = a.workspace = 1 << 20   # aligned, never read
+    a.workspace_bytes = l3.l3_decode_workspace_size(64)
+    a.out_kind = 0
+    assert l3.l3_decode_launches(a) == 1
+    a.n = 32
+    assert l3.l3_decode_launches(a) == 1
+    a.n = 33
+    assert l3.l3_decode_launches(a) == 2
+    a.n = 8
+    a.flags = L3_DECODE_LAYOUT_HWC
+    assert l3.l3_decode_launches(a) == 2
+    a.flags = L3_DECODE_HINT_WIDE
+    assert l3.l3_decode_launches(a) == 2
 
 
 def test_no_cpu_fallback_without_cuda(lib):
