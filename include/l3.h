@@ -130,9 +130,8 @@ uint64_t l3_decode_workspace_size(int32_t n);
  * row-header chain, delta unpack, row-parallel custom Paeth, store / fused normalise;
  * a2-a6) is launched as its programmatic dependent: its blocks are resident and set
  * up before a1 ends and start decoding as soon as a1's results are visible. Planar
- * batches of up to 32 images (no crop, no HWC, no wide hint) run a1 inside every
- * decoder block instead (one launch). The last decoder block writes the per-image
- * status (a7).
+ * batches of up to 32 images (no crop, no HWC) run a1 inside every decoder block
+ * instead (one launch). The last decoder block writes the per-image status (a7).
  * The workspace must be zero-filled before its first use (e.g. cudaMemsetAsync);
  * every call leaves it zero-filled again, so it can be reused without host work.
  */
@@ -157,7 +156,7 @@ l3_status_t l3_load_decode_batch(const l3_decode_args* args, const void* host_sr
 int32_t l3_decode_kernels_per_call(void);
 
 /* Kernels the l3_decode_batch call with these arguments launches: 1 when a1 runs inside the decode
- * grid (planar, not crop, not HWC, no wide hint on u8, n <= 32), 2 otherwise, 0 for n == 0; -1 if the
+ * grid (planar, not crop, not HWC, n <= 32), 2 otherwise, 0 for n == 0; -1 if the
  * arguments are invalid (the same checks as l3_decode_batch). Host-only, no device work. */
 int32_t l3_decode_launches(const l3_decode_args* a);
 

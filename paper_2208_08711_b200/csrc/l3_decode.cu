@@ -707,14 +707,12 @@ cudaError_t launch_parse(const l3_decode_args* a, cudaStream_t s, bool accept_va
 }
 
 // Does this call run a1 inside the decode CTAs (one launch) rather than as its own one-block launch?
-// Planar (not crop, not HWC), narrow (u8 without the wide hint, or fp32) batches of <= kA1InMaxN images.
+// Planar (not crop, not HWC) batches of <= kA1InMaxN images (narrow or wide kernel).
 bool a1_in_cta_call(const l3_decode_args* a) {
   static const int a1in_max = getenv("L3_A1IN_MAX") ? atoi(getenv("L3_A1IN_MAX")) : kA1InMaxN;   // dev A/B
-  const bool f32 = a->out_kind == L3_OUT_F32;
   const bool crop = a->crops != nullptr;
   const bool hwc = (a->flags & L3_DECODE_LAYOUT_HWC) != 0;
-  const bool wide = !crop && !f32 && (a->flags & L3_DECODE_HINT_WIDE);
-  return !hwc && !crop && !wide && a->n <= min(a1in_max, kA1InMaxN);
+  return !hwc && !crop && a->n <= min(a1in_max, kA1InMaxN);
 }
 
 // The whole hot path in ONE persistent launch (grid = SMs x resident CTAs, or fewer CTAs when the

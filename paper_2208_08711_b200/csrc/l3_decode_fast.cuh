@@ -749,17 +749,36 @@ namespace l3 {
 // a1 inside a decode CTA (n <= kA1InMaxN = 32, warp 0): the same header parse and decomposition as
 // l3_prep_kernel's, kept in this CTA's shared memory: compact descriptors and the
 // exclusive task prefixes of the two classes (N <= 128, N > 128), totals at [n].
+// WIDE: the wide kernel's decomposition (parse_phase): images whose class-0 units start within the
+// batch's last tail_units units run as 1-patch tasks (the tail zone), the others keep the 8-column modes.
+template <bool WIDE>
 __device__ __forceinline__ void a1_in_cta(const ParseParams& pp, int lane, uint32_t* pre0, uint32_t* pre1,
                                           A1Compact* a1d) {
   uint32_t t0 = 0, t1 = 0;
+  ImgDesc d;
+  int st = L3_E_INVALID_ARGUMENT;
+  uint64_t units = 0;
   if (lane < pp.n) {
-    ImgDesc d;
-    const int st = parse_header<false, false>(pp, lane, d);
+    st = parse_header<false, false>(pp, lane, d);
+    if (st == L3_OK && d.mode != 3) units = 3ull * d.P;
+  }
+  uint64_t uex = 0, total_units = 0;
+  if (WIDE) {   // exclusive scan of the class-0 units over the batch
+    uint64_t iu = units;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t v = __shfl_up_sync(0xffffffffu, iu, o);
+      if (lane >= o) iu += v;
+    }
+    uex = iu - units;
+    total_units = __shfl_sync(0xffffffffu, iu, 31);
+  }
+  if (lane < pp.n) {
     A1Compact c = {};
     c.st = st;
     if (st == L3_OK) {
-      if (d.mode == 1 || d.mode == 2) {   // the narrow kernels: every 33 <= N <= 128 unit is a 1-patch task
-        d.mode = 4;
+      if ((d.mode == 1 || d.mode == 2) && (!WIDE || uex + units + pp.tail_units > total_units)) {
+        d.mode = 4;   // narrow kernels: every 33 <= N <= 128 unit is a 1-patch task; wide: the tail zone
         d.L = 32;
         d.G = 1;
       }
@@ -833,9 +852,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, WIDE ? 4 : (CROP ? L3_CROP_
   uint32_t* const a1_pre0 = reinterpret_cast<uint32_t*>(sh_prefix);
   uint32_t* const a1_pre1 = a1_pre0 + 34;
   A1Compact* const a1_desc = reinterpret_cast<A1Compact*>(sh_prefix + 34);
-  const bool a1in = !CROP && !WIDE && p.a1in != 0;
+  const bool a1in = !CROP && p.a1in != 0;
   if (a1in) {   // a1 inside this CTA (launch_decode_batch: n <= kA1InMaxN, no a1 launch)
-    if (warp == 0) a1_in_cta(p.pp, lane, a1_pre0, a1_pre1, a1_desc);
+    if (warp == 0) a1_in_cta<WIDE>(p.pp, lane, a1_pre0, a1_pre1, a1_desc);
     __syncthreads();
   } else {
     // ---- a1 ran in the preceding l3_prep_kernel (PDL): wait until its results are visible
