@@ -218,6 +218,41 @@ def test_fault_injection_status_parity(seed):
             assert (st[i], bad[i]) == (rst, rbad), (dtype, wide, layout, i, st[i], bad[i], rst, rbad)
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_a1_launch_modes_agree(seed):
+    """The same corrupted batch through both a1 modes: inside every decode CTA (n <= 32, one launch) and
+    the a1 kernel + PDL (the batch repeated to n > 32): statuses, bad units and pixels equal the oracle's."""
+    from paper_2208_08711_b200 import l3
+    rng = np.random.default_rng(100 + seed)
+    H, W = int(rng.integers(20, 200)), int(rng.integers(20, 300))
+    files, shapes = [], []
+    for N in (32, 64, 128, 200):   # every decode mode incl. the generic N > 128 path
+        im = l3synth.natural(H, W, seed + N, 3.0)
+        f = l3ref.encode(im, N=N)
+        P = (-(-W // N)) * (-(-H // N))
+        v = _corrupt_variants(rng, f, P)
+        files += [v[0], v[3], v[4], v[5], v[-1], f]   # header, truncation, offsets, data flips, k = 0, valid
+    shapes = [(H, W)] * len(files)
+    assert len(files) <= 32
+    big = files * (-(-40 // len(files)))   # > 32 images: the a1 kernel path
+    for dtype, wide in ((torch.uint8, False), (torch.uint8, True), (torch.float32, False)):
+        for fs in (files, big):
+            out, st, bad, _, _, _ = gpu_decode(fs, [(H, W)] * len(fs), dtype=dtype, wide=wide)
+            for i, fi in enumerate(fs):
+                rst, rbad, rpix, _ = l3ref.decode(fi, exp_shape=(H, W))
+                assert (st[i], bad[i]) == (rst, rbad), (dtype, wide, len(fs), i, st[i], bad[i], rst, rbad)
+                if rst == 0 and dtype == torch.uint8:
+                    assert np.array_equal(out[i], np.asarray(rpix).reshape(3, H, W)), (wide, len(fs), i)
+    # the launch count that l3_decode_launches reports for the two modes
+    dec = BatchDecoder(len(big))
+    src, offs = pack_files(big)
+    sh = torch.tensor(np.array([(H, W)] * len(big), np.int32), device="cuda")
+    o = torch.empty(len(big) * 3 * H * W, dtype=torch.uint8, device="cuda")
+    assert l3.l3_decode_launches(dec.args(src, offs, sh, o)) == 2
+    src, offs = pack_files(files)
+    assert l3.l3_decode_launches(dec.args(src, offs, sh[:len(files)].contiguous(), o)) == 1
+
+
 def test_shape_mismatch_is_corrupt_header():
     im = l3synth.natural(40, 50, 1, 1.0)
     f = l3ref.encode(im)
